@@ -1,0 +1,156 @@
+/*
+ * qqq_b200.h — C ABI of the B200-native (sm_100a) W4A8 hot path of QQQ
+ * (arXiv 2406.09904). Plain pointers and sizes only; every device pointer is
+ * caller-allocated (torch, or any CUDA allocator); every call is asynchronous
+ * on the given stream and stateless ("pure functions").
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/qqq/<file>:<line>). Return value: QQQ_OK or one of
+ * the QQQ_ERR_* codes, which the host layer maps to the reference's exception
+ * classes (errors.py:4-33). Data-dependent errors the reference raises
+ * (non-finite activations, out-of-range codes, bad padding, overflowing fused
+ * scales) are reported through a caller-owned device int32 status word
+ * (QQQ_STAT_* bits, atomically OR-ed) that the host checks after its sync.
+ *
+ * Library: paper_2406_09904_b200/lib/libqqq_b200.so (nvcc -gencode
+ * arch=compute_100a,code=sm_100a). Weight-layout and kernel design: DESIGN.md.
+ */
+#ifndef QQQ_B200_H
+#define QQQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* qqq_stream_t; /* == cudaStream_t */
+
+enum {
+  QQQ_OK = 0,
+  QQQ_ERR_SHAPE = 1,       /* ShapeError */
+  QQQ_ERR_DATA = 2,        /* DataError */
+  QQQ_ERR_CONFIG = 3,      /* ConfigError */
+  QQQ_ERR_CORRUPTION = 4,  /* CorruptionError */
+  QQQ_ERR_CUDA = 5,        /* launch / driver failure */
+  QQQ_ERR_UNSUPPORTED = 6  /* shape outside the kernel's contract (host re-lays out) */
+};
+
+enum {
+  QQQ_STAT_NONFINITE = 1,   /* quantize.py:85-89 DataError */
+  QQQ_STAT_CODE_RANGE = 2,  /* quantize.py:181-182 DataError */
+  QQQ_STAT_PAD_NIBBLE = 4,  /* quantize.py:206-207 CorruptionError */
+  QQQ_STAT_SCALE_INF = 8,   /* gemm.py:67-68 ConfigError */
+  QQQ_STAT_NEED_CLAMP = 16, /* repack: FusedDequantQuant clamp needed -> I8 layout */
+  QQQ_STAT_TINY_SCALE = 32  /* repack: s* < 2^-10 -> I8 layout */
+};
+
+enum { QQQ_MODE_PC = 0, QQQ_MODE_PG = 1, QQQ_MODE_I8 = 2 };
+
+/* ---- activations -------------------------------------------------------- */
+
+/* quant_act_per_token (quantize.py:92-100). x: M x K row-major (row stride ldx
+ * elements), dtype 0=f16 1=f32 2=f64. q: int8 M x K (row stride ldq bytes),
+ * s_a: f64[M]. Bit-exact with the reference (ties included). */
+int qqq_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
+                  double* s_a, int32_t* status_dev, qqq_stream_t stream);
+
+/* ---- offline weight preparation ----------------------------------------- */
+
+/* quant_weight_per_channel (quantize.py:111-123) when group <= 0, else the
+ * per-group code/scale step of quant_weight_per_group (quantize.py:126-149).
+ * w: f64 K x N; codes: int8 K x N; scales: f64 [K/group or 1] x N. */
+int qqq_quant_weight(const double* w, int64_t K, int64_t N, int64_t group, int8_t* codes, double* scales,
+                     int32_t* status_dev, qqq_stream_t stream);
+
+/* requant_scale (quantize.py:152-168): s_wc f64[N] from codes and s_wg [G x N]. */
+int qqq_requant_scale(const int8_t* codes, const double* s_wg, int64_t K, int64_t N, int64_t G, double* s_wc,
+                      qqq_stream_t stream);
+
+/* pack_i4 / unpack_i4 (quantize.py:171-208). packed: uint8 ceil(K/2) x N. */
+int qqq_pack_i4(const int8_t* codes, int64_t K, int64_t N, uint8_t* packed, int32_t* status_dev, qqq_stream_t stream);
+int qqq_unpack_i4(const uint8_t* packed, int64_t rows, int64_t N, int8_t* codes, int32_t* status_dev,
+                  qqq_stream_t stream);
+
+/* FusedScales.from_quantized, per-group branch (gemm.py:65-69): s_star binary16
+ * bits [G x N] = f16(s_wg / s_wc). (Per-channel s_w/16 is an exact host-side
+ * tensor op.) */
+int qqq_fused_scales_pg(const double* s_wg, const double* s_wc, int64_t G, int64_t N, uint16_t* s_star,
+                        int32_t* status_dev, qqq_stream_t stream);
+
+/* dequantize_ref (quantize.py:211-217): out f64 K x N = codes * scale
+ * (group <= 0: per-channel scales[N]; else scales[(k/group), n]). */
+int qqq_dequantize(const int8_t* codes, int64_t K, int64_t N, int64_t group, const double* scales, double* out,
+                   qqq_stream_t stream);
+
+/* ---- one-time repack into the tcgen05 kernel layout ---------------------- */
+
+size_t qqq_repacked_weight_bytes(int mode, int64_t K, int64_t N);
+size_t qqq_repacked_scale_bytes(int64_t K, int64_t N, int64_t group);
+
+/* QQQ_MODE_PC / QQQ_MODE_PG nibble layouts from the reference pack_i4 bytes. */
+int qqq_repack_weights(const uint8_t* packed, int64_t K, int64_t N, int mode, void* out, qqq_stream_t stream);
+
+/* QQQ_MODE_I8 layout from an int8 K x N matrix (w8), or from pack_i4 bytes +
+ * s_star via the reference's exact scalar FusedDequantQuant (gemm.py:110-127). */
+int qqq_repack_weights_i8(const int8_t* w8, const uint8_t* packed, const uint16_t* s_star, int64_t group, int64_t K,
+                          int64_t N, void* out, qqq_stream_t stream);
+
+/* s_star [K/group x N] -> per-tile layout; sets QQQ_STAT_NEED_CLAMP /
+ * QQQ_STAT_TINY_SCALE in flags_dev if the fast HFMA2 path is not provably exact. */
+int qqq_repack_scales(const uint16_t* s_star, int64_t K, int64_t N, int64_t group, void* out, int32_t* flags_dev,
+                      qqq_stream_t stream);
+
+/* ---- the W4A8 GEMM ------------------------------------------------------- */
+
+/* Caller-provided zero-initialised workspace; the kernels leave it zeroed. */
+size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
+
+/* w4a8_gemm_per_channel (gemm.py:173-185): y f16 M x N = f16((acc*s_a)*s_w_folded),
+ * acc = aq . (16*q). acc_opt (int32 M x N) is written when non-NULL. aq must be
+ * 16-byte aligned with ldq % 16 == 0. */
+int qqq_w4a8_gemm_pc(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
+                     const double* s_w_folded, int64_t M, int64_t N, int64_t K, void* y, int64_t ldy, int32_t* acc_opt,
+                     int64_t ldacc, void* workspace, size_t ws_bytes, qqq_stream_t stream);
+
+/* w4a8_gemm_per_group (gemm.py:188-203): acc = aq . FusedDequantQuant(q, s*),
+ * y = f16((acc*s_a)*s_wc). group in {32, 64, 128} or a multiple of 256. */
+int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
+                     const void* s_star_repacked, int64_t group, const double* s_wc, int64_t M, int64_t N, int64_t K,
+                     void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
+                     qqq_stream_t stream);
+
+/* Generic form (mode PC/PG/I8) with an optional tile-plan override; I8 with
+ * s_col == NULL is gemm_i8_i32 (gemm.py:145-154, acc only). */
+typedef struct qqq_gemm_config {
+  int ntok;  /* tokens per UMMA tile: 16/32/64/128/256, 0 = auto */
+  int grid;  /* CTAs for stream-K, 0 = auto */
+  int split; /* -1 auto, 0 whole tiles, 1 stream-K */
+} qqq_gemm_config;
+
+int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
+                     const void* sc_repacked, int64_t group, const double* s_col, int64_t M, int64_t N, int64_t K,
+                     void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
+                     const qqq_gemm_config* cfg, qqq_stream_t stream);
+
+/* ---- conversion test hooks (the exact device functions the GEMM uses) ---- */
+
+/* fused_dequant_quant (gemm.py:110-127): word_path=0 scalar reference branch
+ * structure; word_path=1 the GEMM's HFMA2/PRMT converter (8 codes per s*). */
+int qqq_test_fused_dequant_quant(const int8_t* q, const uint16_t* s_star, int8_t* out, int64_t n, int word_path,
+                                 qqq_stream_t stream);
+/* fast_i4_to_i8 (gemm.py:81-85) via the GEMM's per-channel shift converter. */
+int qqq_test_pc_convert(const int8_t* q, int8_t* out, int64_t n, qqq_stream_t stream);
+/* fast_f16_to_i8 (gemm.py:99-107). */
+int qqq_test_fast_f16_to_i8(const uint16_t* bits, int8_t* out, int64_t n, qqq_stream_t stream);
+
+/* ---- misc ---------------------------------------------------------------- */
+int qqq_device_ok(void); /* QQQ_OK iff the current device is sm_100 */
+const char* qqq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QQQ_B200_H */

@@ -1,0 +1,168 @@
+// Per-token symmetric INT8 activation quantization on B200.
+//
+// Reference: pkg/src/qqq/quantize.py:92-100 (quant_act_per_token)
+//   m = max_k |x[t,k]| ; s = m/127 (f64) or 1.0 if m == 0
+//   q = clip(rint(x / s), -127, 127)       (f64 divide, half-even rint)
+//   non-finite input -> DataError (quantize.py:85-89)
+//
+// One CTA per token row: a vectorised 16-byte absmax pass (warp shuffles +
+// shared-memory block reduce) followed by a quantize pass that re-reads the
+// row from L1/L2 and writes 16-byte int8 vectors.
+//
+// Bit-exactness for fp16 input: the fast path
+// computes t = (x*127)/m in fp32 (x*127 is exact, one RN divide, so
+// |t - x*127/m| <= 127*2^-24). Whenever t is within 1e-3 of a half-integer we
+// recompute the reference formula rint(x / (m/127.0)) in f64 verbatim, so the
+// result equals the reference on every input, ties included (the reference is
+// not half-even on exact ties because of its double rounding). f32/f64 inputs
+// always take the verbatim f64 formula.
+#include <type_traits>
+
+#include "qqq_common.cuh"
+
+namespace qqq {
+
+template <typename T>
+QQQ_DEVICE double to_f64(T v);
+QQQ_DEVICE float absval(__half v) { return fabsf(__half2float(v)); }
+QQQ_DEVICE float absval(float v) { return fabsf(v); }
+QQQ_DEVICE double absval(double v) { return fabs(v); }
+QQQ_DEVICE bool is_bad(float a) { return !(a <= 3.4028234663852886e38f); }
+QQQ_DEVICE bool is_bad(double a) { return !(a <= 1.7976931348623157e308); }
+template <>
+QQQ_DEVICE double to_f64<__half>(__half v) { return (double)__half2float(v); }
+template <>
+QQQ_DEVICE double to_f64<float>(float v) { return (double)v; }
+template <>
+QQQ_DEVICE double to_f64<double>(double v) { return v; }
+
+QQQ_DEVICE int8_t quant_code_exact(double x, double s) {
+  double r = rint(x / s);
+  r = fmin(fmax(r, -127.0), 127.0);
+  return (int8_t)(int)r;
+}
+
+// fp16 fast path; inv = RN(127/m) in fp32 (m = row absmax > 0), s the f64
+// scale. |x*inv - x*127/m| <= 2*127*2^-24 < 2e-5, far inside the 1e-3 band.
+QQQ_DEVICE int8_t quant_code_f16(float x, float inv, double s) {
+  float t = x * inv;
+  float r = rintf(t);
+  float d = fabsf(fabsf(t - r) - 0.5f);
+  if (d < 1e-3f) return quant_code_exact((double)x, s);
+  r = fminf(fmaxf(r, -127.0f), 127.0f);
+  return (int8_t)(int)r;
+}
+
+template <int kThreads, typename Acc>
+QQQ_DEVICE Acc block_max(Acc v, Acc* red) {
+  for (int o = 16; o > 0; o >>= 1) { Acc t = __shfl_xor_sync(0xffffffffu, v, o); v = t > v ? t : v; }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = (l < kThreads / 32) ? red[l] : Acc(0);
+    for (int o = 16; o > 0; o >>= 1) { Acc t = __shfl_xor_sync(0xffffffffu, v, o); v = t > v ? t : v; }
+    if (l == 0) red[0] = v;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+template <typename T, int kThreads>
+__global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict__ x, int64_t K, int64_t ldx,
+                                                              int8_t* __restrict__ q, int64_t ldq,
+                                                              double* __restrict__ s_out, int32_t* status) {
+  using Acc = typename std::conditional<sizeof(T) == 8, double, float>::type;
+  __shared__ Acc red[32];
+  const int64_t row = blockIdx.x;
+  const T* xr = x + row * ldx;
+  int8_t* qr = q + row * ldq;
+
+  // ---- pass 1: absmax + finiteness -------------------------------------------------
+  Acc m = Acc(0);
+  bool bad = false;
+  constexpr int kVec = 16 / sizeof(T);
+  const bool vec_ok = (K % kVec == 0) && ((reinterpret_cast<uintptr_t>(xr) & 15) == 0);
+  if (vec_ok) {
+    const int64_t nv = K / kVec;
+    const uint4* xv = reinterpret_cast<const uint4*>(xr);
+    for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
+      uint4 pk = __ldg(xv + i);
+      const T* e = reinterpret_cast<const T*>(&pk);
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        Acc a = absval(e[j]);
+        bad |= is_bad(a);  // inf or NaN
+        m = a > m ? a : m;
+      }
+    }
+  } else {
+    for (int64_t i = threadIdx.x; i < K; i += kThreads) {
+      Acc a = absval(xr[i]);
+      bad |= is_bad(a);
+      m = a > m ? a : m;
+    }
+  }
+  if (__syncthreads_or(bad)) {
+    if (threadIdx.x == 0) atomicOr(status, kStatNonFinite);
+  }
+  m = block_max<kThreads, Acc>(m, red);
+  const double s = (m > Acc(0)) ? (double)m / 127.0 : 1.0;
+  if (threadIdx.x == 0) s_out[row] = s;
+
+  // ---- pass 2: codes ----------------------------------------------------------------
+  const bool zero_row = !(m > Acc(0));
+  const float inv = zero_row ? 0.0f : 127.0f / (float)m;  // fp16 path only
+  auto code = [&](T v) -> int8_t {
+    if (zero_row) return 0;
+    if constexpr (sizeof(T) == 2) {
+      return quant_code_f16(__half2float(v), inv, s);
+    } else {
+      return quant_code_exact(to_f64<T>(v), s);
+    }
+  };
+  const bool qvec_ok = vec_ok && (K % 16 == 0) && ((reinterpret_cast<uintptr_t>(qr) & 15) == 0);
+  if (qvec_ok) {
+    // 16 codes per thread-iteration: 16 * sizeof(T) bytes in, 16 bytes out
+    const int64_t n16 = K / 16;
+    for (int64_t i = threadIdx.x; i < n16; i += kThreads) {
+      alignas(16) int8_t out[16];
+#pragma unroll
+      for (int h = 0; h < (int)sizeof(T); ++h) {
+        uint4 pk = __ldg(reinterpret_cast<const uint4*>(xr + i * 16) + h);
+        const T* e = reinterpret_cast<const T*>(&pk);
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) out[h * kVec + j] = code(e[j]);
+      }
+      *reinterpret_cast<uint4*>(qr + i * 16) = *reinterpret_cast<const uint4*>(out);
+    }
+  } else {
+    for (int64_t i = threadIdx.x; i < K; i += kThreads) qr[i] = code(xr[i]);
+  }
+}
+
+}  // namespace qqq
+
+using namespace qqq;
+
+extern "C" int qqq_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
+                             double* s_a, int32_t* status_dev, cudaStream_t stream) {
+  if (M < 0 || K <= 0 || ldx < K || ldq < K) return kErrShape;
+  if (M == 0) return kOk;
+  constexpr int kT = 256;
+  dim3 grid((unsigned)M);
+  switch (x_dtype) {
+    case 0:
+      act_quant_kernel<__half, kT><<<grid, kT, 0, stream>>>((const __half*)x, K, ldx, q, ldq, s_a, status_dev);
+      break;
+    case 1:
+      act_quant_kernel<float, kT><<<grid, kT, 0, stream>>>((const float*)x, K, ldx, q, ldq, s_a, status_dev);
+      break;
+    case 2:
+      act_quant_kernel<double, kT><<<grid, kT, 0, stream>>>((const double*)x, K, ldx, q, ldq, s_a, status_dev);
+      break;
+    default:
+      return kErrConfig;
+  }
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+}

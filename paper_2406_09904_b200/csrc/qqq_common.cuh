@@ -1,0 +1,274 @@
+// Shared device helpers for the B200 (sm_100a) W4A8 path: PTX wrappers for
+// mbarrier / TMA / tcgen05, and the bit-exact INT4 -> INT8 conversions of the
+// QQQ dataflows (reference: pkg/src/qqq/gemm.py:81-142).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qqq_b200.h"  // the C ABI these kernels implement
+
+#define QQQ_DEVICE __device__ __forceinline__
+
+namespace qqq {
+
+// ----------------------------------------------------------------------------
+// Status codes shared with include/qqq_b200.h
+// ----------------------------------------------------------------------------
+enum : int {
+  kOk = 0,
+  kErrShape = 1,
+  kErrData = 2,
+  kErrConfig = 3,
+  kErrCorruption = 4,
+  kErrCuda = 5,
+  kErrUnsupported = 6,
+};
+
+// device-side status bits (written with atomicOr into a caller-owned int32)
+enum : int {
+  kStatNonFinite = 1,     // quant_act_per_token / weight quantizers: DataError
+  kStatCodeRange = 2,     // pack_i4: code outside [-8, 7]: DataError
+  kStatPadNibble = 4,     // unpack_i4: nonzero odd-K padding: CorruptionError
+  kStatScaleInf = 8,      // FusedScales.from_quantized: s* overflows binary16
+  kStatNeedClamp = 16,    // repack: some s* needs the FusedDequantQuant clamp
+  kStatTinyScale = 32,    // repack: some s* < 2^-10 (s*/16 inexact)
+};
+
+// ----------------------------------------------------------------------------
+// Generic small helpers
+// ----------------------------------------------------------------------------
+QQQ_DEVICE uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+QQQ_DEVICE uint32_t lane_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));
+  return r;
+}
+
+QQQ_DEVICE bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// ----------------------------------------------------------------------------
+// mbarrier
+// ----------------------------------------------------------------------------
+QQQ_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+QQQ_DEVICE void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+QQQ_DEVICE void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+QQQ_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+// Parity wait. A watchdog turns a pipeline deadlock into a trapped launch
+// (cudaErrorLaunchFailure) after ~2^24 polls (seconds) instead of hanging the GPU.
+QQQ_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+#pragma unroll 1
+  for (uint32_t n = 0;; ++n) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+#ifndef QQQ_NO_WATCHDOG
+    if (n > (1u << 24)) __trap();
+#endif
+  }
+}
+
+// ----------------------------------------------------------------------------
+// TMA / bulk copies (async proxy)
+// ----------------------------------------------------------------------------
+QQQ_DEVICE void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+QQQ_DEVICE void tma_load_2d(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+QQQ_DEVICE void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+QQQ_DEVICE void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ----------------------------------------------------------------------------
+// tcgen05 (5th-gen tensor core, TMEM accumulators)
+// ----------------------------------------------------------------------------
+QQQ_DEVICE void tmem_alloc(uint32_t* smem_result, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_result)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+QQQ_DEVICE void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+QQQ_DEVICE void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+QQQ_DEVICE void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// D[tmem] (+)= A[smem] * B[smem]^T, int8 x int8 -> int32 (kind::i8)
+QQQ_DEVICE void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+QQQ_DEVICE void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+QQQ_DEVICE void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// 32 lanes x 32-bit, 16 consecutive columns per thread
+QQQ_DEVICE void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+// Shared-memory matrix descriptor (tcgen05 "version 1" format).
+//   layout: 0 = SWIZZLE_NONE (canonical interleaved core matrices), 2 = SWIZZLE_128B
+QQQ_DEVICE uint64_t make_smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version = 1 (sm_100)
+  d |= (uint64_t)(layout & 0x7) << 61;
+  return d;
+}
+
+// Instruction descriptor for kind::i8: s8 x s8 -> s32, both operands K-major.
+__host__ __device__ constexpr uint32_t make_idesc_i8(uint32_t M, uint32_t N) {
+  return (2u << 4)            // c_format = S32
+         | (1u << 7)          // a_format = signed int8
+         | (1u << 10)         // b_format = signed int8
+         | ((N >> 3) << 17)   // n_dim
+         | ((M >> 4) << 24);  // m_dim
+}
+
+// ----------------------------------------------------------------------------
+// QQQ conversions (bit-exact with gemm.py)
+// ----------------------------------------------------------------------------
+
+// Per-channel FastINT4toINT8 (gemm.py:81-85, applied as `codes*16` at :180):
+// one 32-bit word of the per-channel kernel layout holds 8 biased nibbles u=q+8;
+// byte j's low nibble is k=4i+j and its high nibble is k=16+4i+j. Returns the
+// two int8x4 words 16*q (low nibbles) and 16*q (high nibbles):
+//   (u << 4) ^ 0x80  ==  16*(u-8) as a two's-complement byte.
+QQQ_DEVICE void pc_convert_word(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  lo = ((w << 4) & 0xF0F0F0F0u) ^ 0x80808080u;
+  hi = (w & 0xF0F0F0F0u) ^ 0x80808080u;
+}
+
+QQQ_DEVICE uint32_t h2_as_u32(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+QQQ_DEVICE __half2 u32_as_h2(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+
+// Per-group FusedDequantQuant (gemm.py:110-142) on one word of the per-group
+// kernel layout. Nibble p sits at bits 4p; pairs (p, p+4) form half2 lanes and
+// cover k = (0,1) p=0, (2,3) p=1, (4,5) p=2, (6,7) p=3 of this word's 8 k's.
+//   FastINT4toFP16: half(0x6400|u) = 1024+u ; minus 1032 -> q exactly
+//   odd pairs use the nibble in place (1024+16u), minus 1152 -> 16q, and are
+//   multiplied by s*/16 (exact when s* >= 2^-10, checked at repack time) so the
+//   single-rounding FMA q*s* + 1152 is computed identically.
+//   FastFP16toINT8: low byte of the fp16 bits, XOR 0x80.
+// kClamp reproduces the reference's out-of-range clamp to [-127, 127]; the
+// repack proves it unnecessary for the weights it accepts on the fast path.
+template <bool kClamp>
+QQQ_DEVICE void pg_convert_word(uint32_t w, __half2 s2, __half2 s2_16, uint32_t& out_lo, uint32_t& out_hi) {
+  const uint32_t kMagic = 0x64006400u;
+  const __half2 k1032 = u32_as_h2(0xE408E408u);  // -1032.0
+  const __half2 k1152 = u32_as_h2(0xE480E480u);  // -1152.0
+  const __half2 kAdd = u32_as_h2(0x64806480u);   // +1152.0
+  uint32_t a = (w & 0x000F000Fu) | kMagic;
+  uint32_t b = (w & 0x00F000F0u) | kMagic;
+  uint32_t w8 = w >> 8;
+  uint32_t c = (w8 & 0x000F000Fu) | kMagic;
+  uint32_t d = (w8 & 0x00F000F0u) | kMagic;
+  __half2 ra = __hfma2(__hadd2(u32_as_h2(a), k1032), s2, kAdd);
+  __half2 rb = __hfma2(__hadd2(u32_as_h2(b), k1152), s2_16, kAdd);
+  __half2 rc = __hfma2(__hadd2(u32_as_h2(c), k1032), s2, kAdd);
+  __half2 rd = __hfma2(__hadd2(u32_as_h2(d), k1152), s2_16, kAdd);
+  if (kClamp) {
+    const __half2 lo = u32_as_h2(0x64016401u);  // 1025
+    const __half2 hi = u32_as_h2(0x64FF64FFu);  // 1279
+    ra = __hmin2(__hmax2(ra, lo), hi);
+    rb = __hmin2(__hmax2(rb, lo), hi);
+    rc = __hmin2(__hmax2(rc, lo), hi);
+    rd = __hmin2(__hmax2(rd, lo), hi);
+  }
+  out_lo = __byte_perm(h2_as_u32(ra), h2_as_u32(rb), 0x6420) ^ 0x80808080u;
+  out_hi = __byte_perm(h2_as_u32(rc), h2_as_u32(rd), 0x6420) ^ 0x80808080u;
+}
+
+// Scalar FusedDequantQuant with the reference's full branch structure
+// (gemm.py:110-127 / vectorized :130-142): fma(q, s*, 1152) in binary16 with a
+// single rounding, then the aligned-window test on the bit pattern.
+QQQ_DEVICE int8_t fused_dequant_quant_scalar(int q, __half s_star) {
+  __half r = __hfma(__int2half_rn(q), s_star, __float2half_rn(1152.0f));
+  uint16_t bits = __half_as_ushort(r);
+  if (bits >= 0x6400 && bits < 0x6500) {
+    int b = (bits & 0xFF) ^ 0x80;
+    int v = b >= 128 ? b - 256 : b;
+    return (int8_t)(v < -127 ? -127 : v);
+  }
+  // prod = q*s* is exact; its sign decides the saturation side
+  float prod = (float)q * __half2float(s_star);
+  return (int8_t)(prod > 0.0f ? 127 : -127);
+}
+
+// FastFP16toINT8 (gemm.py:99-107): fma with multiplicand 1.0, low byte ^ 0x80
+QQQ_DEVICE int8_t fast_f16_to_i8(__half x) {
+  __half r = __hadd(x, __float2half_rn(1152.0f));
+  int b = (__half_as_ushort(r) & 0xFF) ^ 0x80;
+  return (int8_t)(b >= 128 ? b - 256 : b);
+}
+
+}  // namespace qqq

@@ -1,0 +1,576 @@
+// B200 (sm_100a) W4A8 GEMM: per-channel and per-group QQQ dataflows on tcgen05.
+//
+// Reference semantics (pkg/src/qqq/gemm.py):
+//   per-channel  (:173-185): w8 = 16*q ; acc = A_i8 . w8 (int32) ;
+//                            y = f16((acc * s_a[t]) * s_w_folded[n])   (f64, one rounding)
+//   per-group    (:188-203): w8 = FusedDequantQuant(q, s*[k/g, n]) ;
+//                            acc = A_i8 . w8 ; y = f16((acc * s_a[t]) * s_wc[n])
+//
+// Design (weight-stationary, tokens on the MMA N axis):
+//   * UMMA M = 128 output channels per tile, UMMA N = NTOK tokens (16..256),
+//     int8 x int8 -> int32 accumulators in TMEM (tcgen05.mma kind::i8).
+//   * Warp roles (512 threads): w0 = TMA/bulk producer, w1 = MMA issuer,
+//     w2 = TMEM allocator, w4-7 = epilogue (one TMEM lane quadrant each),
+//     w8-15 = INT4->INT8 converters (shift for PC, HFMA2 magic-number
+//     FusedDequantQuant for PG) writing the canonical no-swizzle K-major
+//     operand into shared memory.
+//   * Activations: 2-D TMA (SWIZZLE_128B, OOB rows zero-filled) of the int8
+//     [M, K] codes; weights: 1-D cp.async.bulk of contiguous repacked k-blocks.
+//   * Work split: stream-K over (tile, k-block) units across the 148 SMs; split
+//     tiles reduce their int32 partials with red.global.add (integer, so the
+//     result is order-free and bit-exact) and the last arriving CTA applies the
+//     epilogue and re-zeroes the workspace. Unsplit tiles go straight to the
+//     epilogue from TMEM (double-buffered accumulators).
+//   * Epilogue: f64 (acc * s_a) * s_col then cvt.rn.f16.f64 -> bit-identical
+//     to the reference's f64 epilogue with a single final rounding.
+#include <cstdio>
+#include <mutex>
+
+#include "qqq_common.cuh"
+#include "qqq_layout.cuh"
+
+namespace qqq {
+
+constexpr int kNumThreads = 512;
+constexpr int kEpiWarp0 = 4, kNumEpiWarps = 4;
+constexpr int kConvWarp0 = 8, kNumConvWarps = 8;
+constexpr int kSmemBudget = 225 * 1024;
+
+struct GemmParams {
+  const uint8_t* w;    // repacked weights (layout in qqq_layout.cuh)
+  const __half* sc;    // PG: repacked s* [n_tiles][G_pad][128]
+  const double* s_a;   // [M]
+  const double* s_col; // [N] s_w_folded (PC) / s_wc (PG); nullptr -> acc only
+  __half* y;
+  int64_t ldy;
+  int32_t* acc;  // optional
+  int64_t ldacc;
+  int32_t* ws;        // [tiles][NTOK][128] int32, zero on entry and exit
+  int32_t* counters;  // [tiles], zero on entry and exit
+  int M, N, K;
+  int n_tiles, tok_tiles, kb_per_tile, slabs, g_pad, group;
+  int64_t units;
+  int aligned_tiles;  // >0: CTA b owns whole tiles [b*aligned_tiles, ...)
+};
+
+template <int MODE, int NTOK, int BK>
+struct Cfg {
+  static constexpr bool kConvert = MODE != kModeI8;
+  static constexpr int kActBytes = NTOK * BK;
+  static constexpr int kWBytes = (MODE == kModeI8) ? BK * 128 : BK * 64;
+  static constexpr int kScBytes = (MODE == kModePG) ? (BK / 32) * 256 : 0;
+  static constexpr int kABytes = BK * 128;
+  static constexpr int kABufs = kConvert ? 2 : 0;
+  static constexpr int kStageBytes = kActBytes + kWBytes + kScBytes;
+  static constexpr int kStagesRaw = (kSmemBudget - 4096 - kABufs * kABytes) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static_assert(kStages >= 2, "shared memory budget too small");
+  static constexpr int kOffAct = 0;
+  static constexpr int kOffW = kOffAct + kStages * kActBytes;
+  static constexpr int kOffSc = kOffW + kStages * kWBytes;
+  static constexpr int kOffA = (kOffSc + kStages * kScBytes + 1023) / 1024 * 1024;
+  static constexpr int kOffBar = kOffA + kABufs * kABytes;
+  static constexpr int kNumBars = 2 * kStages + 2 * kABufs + 4;
+  static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // +1024 alignment slack
+  static constexpr uint32_t kTmemCols = (2 * NTOK <= 32) ? 32 : (2 * NTOK <= 64) ? 64 : (2 * NTOK <= 128) ? 128
+                                        : (2 * NTOK <= 256) ? 256 : 512;
+  static constexpr uint32_t kIdesc = make_idesc_i8(128, NTOK);
+  static_assert(NTOK % 16 == 0 && NTOK >= 16 && NTOK <= 256, "invalid UMMA N");
+  static_assert(BK % 128 == 0, "BK must be a multiple of the 128-byte swizzle atom");
+};
+
+QQQ_DEVICE void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+QQQ_DEVICE __half f64_to_f16_rn(double v) {
+  unsigned short h;
+  asm("cvt.rn.f16.f64 %0, %1;" : "=h"(h) : "d"(v));
+  return __ushort_as_half(h);
+}
+
+QQQ_DEVICE void red_add_s32(int32_t* p, int32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+QQQ_DEVICE int32_t ld_cg_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// Segment iterator: the contiguous unit range of this CTA split at tile borders.
+struct SegIter {
+  int64_t u, u1;
+  int kbt;
+  QQQ_DEVICE bool next(int& tile, int& kb0, int& kb1) {
+    if (u >= u1) return false;
+    tile = (int)(u / kbt);
+    kb0 = (int)(u % kbt);
+    int64_t rem = u1 - u;
+    kb1 = (int)((kbt - kb0) < rem ? kbt : kb0 + rem);
+    u += kb1 - kb0;
+    return true;
+  }
+};
+
+QQQ_DEVICE SegIter make_iter(const GemmParams& p) {
+  SegIter it;
+  it.kbt = p.kb_per_tile;
+  if (p.aligned_tiles > 0) {
+    int64_t t0 = (int64_t)blockIdx.x * p.aligned_tiles;
+    int64_t tiles = (int64_t)p.n_tiles * p.tok_tiles;
+    int64_t t1 = t0 + p.aligned_tiles < tiles ? t0 + p.aligned_tiles : tiles;
+    it.u = t0 * p.kb_per_tile;
+    it.u1 = (t1 > t0 ? t1 : t0) * p.kb_per_tile;
+  } else {
+    it.u = (int64_t)blockIdx.x * p.units / gridDim.x;
+    it.u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
+  }
+  return it;
+}
+
+template <int MODE, int NTOK, int BK>
+__global__ void __launch_bounds__(kNumThreads, 1)
+    w4a8_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const GemmParams p) {
+  using C = Cfg<MODE, NTOK, BK>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::kStages;
+  uint64_t* a_full = bars + 2 * C::kStages;
+  uint64_t* a_empty = a_full + C::kABufs;
+  uint64_t* acc_full = a_empty + C::kABufs;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+  volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::kConvert ? kNumConvWarps + 1 : 1);
+    }
+    for (int b = 0; b < C::kABufs; ++b) {
+      mbar_init(&a_full[b], kNumConvWarps);
+      mbar_init(&a_empty[b], 1);
+    }
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&acc_full[j], 1);
+      mbar_init(&acc_empty[j], kNumEpiWarps);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 0 && lane == 0) tma_prefetch_desc(&act_map);
+  if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ======================= TMA / bulk producer =======================
+    if (lane == 0) {
+      SegIter si = make_iter(p);
+      int tile, kb0, kb1;
+      uint32_t it = 0;
+      while (si.next(tile, kb0, kb1)) {
+        const int n_tile = tile / p.tok_tiles;
+        const int tok0 = (tile % p.tok_tiles) * NTOK;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % C::kStages;
+          mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], C::kStageBytes);
+          uint8_t* act = smem + C::kOffAct + s * C::kActBytes;
+#pragma unroll
+          for (int j = 0; j < BK / 128; ++j)
+            tma_load_2d(act + j * NTOK * 128, &act_map, kb * BK + j * 128, tok0, &full[s]);
+          const int64_t slab0 = (int64_t)n_tile * p.slabs + (int64_t)kb * (BK / 32);
+          const int64_t wofs = slab0 * (MODE == kModeI8 ? 4096 : 2048);
+          bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + wofs, C::kWBytes, &full[s]);
+          if constexpr (MODE == kModePG) {
+            // groups covered by this k-block (g <= BK: BK/g groups; g > BK: one)
+            const int g = p.group;
+            const int gfirst = (int)(((int64_t)kb * BK) / g);
+            const int ngroups = g <= BK ? BK / g : 1;
+            const __half* src = p.sc + ((int64_t)n_tile * p.g_pad + gfirst) * 128;
+            // always move the full per-stage scale footprint so expect_tx is constant
+            const int bytes = ngroups * 256;
+            bulk_g2s(smem + C::kOffSc + s * C::kScBytes, src, bytes, &full[s]);
+            if (bytes < C::kScBytes) {
+              // pad the transaction count with a dummy re-read of the same bytes
+              int rem = C::kScBytes - bytes;
+              while (rem > 0) {
+                int b = rem < bytes ? rem : bytes;
+                bulk_g2s(smem + C::kOffSc + s * C::kScBytes + (C::kScBytes - rem), src, b, &full[s]);
+                rem -= b;
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer ============================
+    if (lane == 0) {
+      SegIter si = make_iter(p);
+      int tile, kb0, kb1;
+      uint32_t it = 0, ait = 0, seg = 0;
+      while (si.next(tile, kb0, kb1)) {
+        const int j = seg & 1;
+        mbar_wait(&acc_empty[j], ((seg >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + j * NTOK;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % C::kStages;
+          mbar_wait(&full[s], (it / C::kStages) & 1);
+          uint32_t a_addr;
+          int b = 0;
+          if constexpr (C::kConvert) {
+            b = ait % C::kABufs;
+            mbar_wait(&a_full[b], (ait / C::kABufs) & 1);
+            a_addr = smem_u32(smem + C::kOffA + b * C::kABytes);
+          } else {
+            a_addr = smem_u32(smem + C::kOffW + s * C::kWBytes);
+          }
+          tc_fence_after();
+          const uint32_t act_addr = smem_u32(smem + C::kOffAct + s * C::kActBytes);
+#pragma unroll
+          for (int kk = 0; kk < BK / 32; ++kk) {
+            // A: canonical K-major, no swizzle: [k16 chunk][128 rows][16 B]
+            const uint64_t a_desc = make_smem_desc(a_addr + kk * 2 * 2048, 2048, 128, 0);
+            // B: TMA SWIZZLE_128B box [NTOK rows][128 B]; 32 B K-steps inside the atom
+            const uint32_t b_addr = act_addr + (kk / 4) * (NTOK * 128) + (kk % 4) * 32;
+            const uint64_t b_desc = make_smem_desc(b_addr, 16, 1024, 2);
+            mma_i8_ss(d_tmem, a_desc, b_desc, C::kIdesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
+          if constexpr (C::kConvert) {
+            mma_commit(&a_empty[b]);
+            ++ait;
+          }
+        }
+        mma_commit(&acc_full[j]);
+        ++seg;
+      }
+    }
+  } else if (warp >= kConvWarp0) {
+    // ====================== INT4 -> INT8 converters ======================
+    if constexpr (C::kConvert) {
+      const int cw = warp - kConvWarp0;
+      SegIter si = make_iter(p);
+      int tile, kb0, kb1;
+      uint32_t it = 0, ait = 0;
+      while (si.next(tile, kb0, kb1)) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it, ++ait) {
+          const int s = it % C::kStages;
+          mbar_wait(&full[s], (it / C::kStages) & 1);
+          const int b = ait % C::kABufs;
+          mbar_wait(&a_empty[b], ((ait / C::kABufs) & 1) ^ 1);
+          const uint8_t* wst = smem + C::kOffW + s * C::kWBytes;
+          uint8_t* abuf = smem + C::kOffA + b * C::kABytes;
+#pragma unroll
+          for (int wu = cw; wu < BK / 8; wu += kNumConvWarps) {
+            const int c = wu >> 2;                  // slab within the k-block
+            const int row = ((wu & 3) << 5) + lane;  // channel within the tile
+            const uint4 v = *reinterpret_cast<const uint4*>(wst + (c * 128 + row) * 16);
+            uint4 o0, o1;
+            if constexpr (MODE == kModePC) {
+              pc_convert_word(v.x, o0.x, o1.x);
+              pc_convert_word(v.y, o0.y, o1.y);
+              pc_convert_word(v.z, o0.z, o1.z);
+              pc_convert_word(v.w, o0.w, o1.w);
+            } else {
+              const int g = p.group;
+              const int lg = g <= BK ? (c * 32) / g : 0;
+              const __half s1 = reinterpret_cast<const __half*>(smem + C::kOffSc + s * C::kScBytes)[lg * 128 + row];
+              const __half2 s2 = __halves2half2(s1, s1);
+              const __half2 s16 = __hmul2(s2, u32_as_h2(0x2C002C00u));  // * 1/16, exact for s* >= 2^-10
+              pg_convert_word<false>(v.x, s2, s16, o0.x, o0.y);
+              pg_convert_word<false>(v.y, s2, s16, o0.z, o0.w);
+              pg_convert_word<false>(v.z, s2, s16, o1.x, o1.y);
+              pg_convert_word<false>(v.w, s2, s16, o1.z, o1.w);
+            }
+            *reinterpret_cast<uint4*>(abuf + ((2 * c) * 128 + row) * 16) = o0;
+            *reinterpret_cast<uint4*>(abuf + ((2 * c + 1) * 128 + row) * 16) = o1;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&a_full[b]);
+            mbar_arrive(&empty[s]);
+          }
+        }
+      }
+    }
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpiWarps) {
+    // ============================== epilogue ==============================
+    const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
+    const int row = q * 32 + lane;
+    SegIter si = make_iter(p);
+    int tile, kb0, kb1;
+    uint32_t seg = 0;
+    while (si.next(tile, kb0, kb1)) {
+      const int j = seg & 1;
+      mbar_wait(&acc_full[j], (seg >> 1) & 1);
+      tc_fence_after();
+      const int n_tile = tile / p.tok_tiles;
+      const int tok0 = (tile % p.tok_tiles) * NTOK;
+      const int n = n_tile * 128 + row;
+      const bool n_ok = n < p.N;
+      const bool whole = (kb0 == 0 && kb1 == p.kb_per_tile);
+      const double s_col = (n_ok && p.s_col) ? p.s_col[n] : 0.0;
+      int32_t* ws_tile = p.ws + (int64_t)tile * NTOK * 128;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NTOK; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(taddr + c0, r);
+        tmem_wait_ld();
+        if (c0 + 16 >= NTOK) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[j]);
+        }
+        if (whole) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int t = tok0 + c0 + i;
+            if (t < p.M && n_ok) {
+              const int32_t a = (int32_t)r[i];
+              if (p.acc) p.acc[(int64_t)t * p.ldacc + n] = a;
+              if (p.s_col) p.y[(int64_t)t * p.ldy + n] = f64_to_f16_rn(((double)a * p.s_a[t]) * s_col);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int t = tok0 + c0 + i;
+            if (t < p.M) red_add_s32(ws_tile + (c0 + i) * 128 + row, (int32_t)r[i]);
+          }
+        }
+      }
+      if (!whole) {
+        __threadfence();
+        named_bar_sync(1, kNumEpiWarps * 32);
+        if (warp == kEpiWarp0 && lane == 0) {
+          const int add = kb1 - kb0;
+          const int old = atomicAdd(p.counters + tile, add);
+          *last_flag = (old + add == p.kb_per_tile) ? 1 : 0;
+        }
+        named_bar_sync(1, kNumEpiWarps * 32);
+        if (*last_flag) {
+          __threadfence();
+          const int tmax = (p.M - tok0) < NTOK ? (p.M - tok0) : NTOK;
+          for (int i = 0; i < tmax; ++i) {
+            const int t = tok0 + i;
+            int32_t* cell = ws_tile + i * 128 + row;
+            const int32_t a = ld_cg_s32(cell);
+            *cell = 0;
+            if (n_ok) {
+              if (p.acc) p.acc[(int64_t)t * p.ldacc + n] = a;
+              if (p.s_col) p.y[(int64_t)t * p.ldy + n] = f64_to_f16_rn(((double)a * p.s_a[t]) * s_col);
+            }
+          }
+          if (warp == kEpiWarp0 && lane == 0) p.counters[tile] = 0;
+        }
+        named_bar_sync(1, kNumEpiWarps * 32);  // last_flag reuse guard
+      }
+      ++seg;
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+struct LaunchPlan {
+  int ntok, bk, grid, aligned_tiles, tok_tiles, n_tiles, kb_per_tile, tiles;
+  int64_t units;
+};
+
+static int pick_ntok(int64_t M) {
+  if (M <= 16) return 16;
+  if (M <= 32) return 32;
+  if (M <= 64) return 64;
+  if (M <= 128) return 128;
+  return 256;
+}
+
+static LaunchPlan make_plan(int64_t M, int64_t N, int64_t K, int force_ntok, int force_grid, int force_split) {
+  LaunchPlan lp{};
+  lp.ntok = force_ntok > 0 ? force_ntok : pick_ntok(M);
+  lp.bk = lp.ntok <= 64 ? 256 : 128;
+  lp.tok_tiles = (int)((M + lp.ntok - 1) / lp.ntok);
+  lp.n_tiles = (int)(round_up(N, kTileN) / kTileN);
+  lp.kb_per_tile = (int)(round_up(K, kKPadTo) / lp.bk);
+  lp.tiles = lp.n_tiles * lp.tok_tiles;
+  lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
+  const int sms = num_sms();
+  // stream-K for small token tiles (cheap int32 fix-up), whole tiles otherwise
+  bool streamk = force_split >= 0 ? force_split == 1 : (lp.ntok <= 64 || lp.tiles < sms / 2);
+  if (streamk) {
+    lp.aligned_tiles = 0;
+    lp.grid = (int)(lp.units < sms ? lp.units : sms);
+    if (force_grid > 0) lp.grid = (int)(force_grid < lp.units ? force_grid : lp.units);
+  } else {
+    int per = (lp.tiles + sms - 1) / sms;
+    lp.aligned_tiles = per;
+    lp.grid = (lp.tiles + per - 1) / per;
+  }
+  return lp;
+}
+
+template <int MODE, int NTOK, int BK>
+static int launch_t(const CUtensorMap& map, const GemmParams& p, int grid, cudaStream_t stream) {
+  using C = Cfg<MODE, NTOK, BK>;
+  auto kern = w4a8_gemm_kernel<MODE, NTOK, BK>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
+      return kErrCuda;
+    attr_set = true;
+  }
+  kern<<<grid, kNumThreads, C::kSmemBytes, stream>>>(map, p);
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+}
+
+template <int MODE>
+static int launch_mode(int ntok, const CUtensorMap& map, const GemmParams& p, int grid, cudaStream_t st) {
+  switch (ntok) {
+    case 16: return launch_t<MODE, 16, 256>(map, p, grid, st);
+    case 32: return launch_t<MODE, 32, 256>(map, p, grid, st);
+    case 64: return launch_t<MODE, 64, 256>(map, p, grid, st);
+    case 128: return launch_t<MODE, 128, 128>(map, p, grid, st);
+    case 256: return launch_t<MODE, 256, 128>(map, p, grid, st);
+    default: return kErrConfig;
+  }
+}
+
+}  // namespace qqq
+
+using namespace qqq;
+
+extern "C" size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  // worst case over configs: every tile of the smallest-padding plan
+  size_t best = 0;
+  for (int nt : {16, 32, 64, 128, 256}) {
+    int64_t tt = (M + nt - 1) / nt;
+    size_t b = (size_t)round_up(N, kTileN) * tt * nt * 4 + (size_t)(round_up(N, kTileN) / kTileN) * tt * 4 + 256;
+    if (b > best) best = b;
+  }
+  return best;
+}
+
+// Generic entry: mode 0 = per-channel (PC), 1 = per-group (PG), 2 = pre-converted int8 (I8).
+extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
+                                const void* sc_repacked, int64_t group, const double* s_col, int64_t M, int64_t N,
+                                int64_t K, void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace,
+                                size_t ws_bytes, const qqq_gemm_config* cfg, cudaStream_t stream) {
+  if (M < 0 || N <= 0 || K <= 0) return kErrShape;
+  if (K > (1 << 16)) return kErrShape;  // gemm.py:49,151
+  if (M == 0) return kOk;
+  if (mode == kModePG && (group <= 0 || !(group % 256 == 0 || (group <= 128 && 128 % group == 0 && group % 32 == 0))))
+    return kErrUnsupported;
+  if (mode == kModePG && !sc_repacked) return kErrConfig;
+  if ((ldq % 16) != 0 || (reinterpret_cast<uintptr_t>(aq) & 15) != 0) return kErrUnsupported;
+  if (s_col && (!y || ldy < N)) return kErrShape;
+  if (!s_col && !acc_opt) return kErrConfig;
+  if (ws_bytes < qqq_gemm_workspace_bytes(M, N, K)) return kErrConfig;
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return kErrCuda;
+
+  LaunchPlan lp = make_plan(M, N, K, cfg ? cfg->ntok : 0, cfg ? cfg->grid : 0, cfg ? cfg->split : -1);
+
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+  cuuint64_t strides[1] = {(cuuint64_t)ldq};
+  cuuint32_t box[2] = {128u, (cuuint32_t)lp.ntok};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)aq, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return kErrCuda;
+
+  GemmParams p{};
+  p.w = (const uint8_t*)w_repacked;
+  p.sc = (const __half*)sc_repacked;
+  p.s_a = s_a;
+  p.s_col = s_col;
+  p.y = (__half*)y;
+  p.ldy = ldy;
+  p.acc = acc_opt;
+  p.ldacc = ldacc;
+  const size_t ws_main = (size_t)lp.tiles * lp.ntok * 128 * 4;
+  p.ws = (int32_t*)workspace;
+  p.counters = (int32_t*)((uint8_t*)workspace + ws_main);
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  p.n_tiles = lp.n_tiles;
+  p.tok_tiles = lp.tok_tiles;
+  p.kb_per_tile = lp.kb_per_tile;
+  p.slabs = (int)(round_up(K, kKPadTo) / kSlabK);
+  p.group = (int)group;
+  p.g_pad = group > 0 ? (int)((round_up(K, kKPadTo) + group - 1) / group) : 0;
+  p.units = lp.units;
+  p.aligned_tiles = lp.aligned_tiles;
+
+  switch (mode) {
+    case kModePC: return launch_mode<kModePC>(lp.ntok, map, p, lp.grid, stream);
+    case kModePG: return launch_mode<kModePG>(lp.ntok, map, p, lp.grid, stream);
+    case kModeI8: return launch_mode<kModeI8>(lp.ntok, map, p, lp.grid, stream);
+    default: return kErrConfig;
+  }
+}
+
+extern "C" int qqq_w4a8_gemm_pc(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
+                                const double* s_w_folded, int64_t M, int64_t N, int64_t K, void* y, int64_t ldy,
+                                int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes, cudaStream_t stream) {
+  return qqq_w4a8_gemm_ex(kModePC, aq, ldq, s_a, w_repacked, nullptr, 0, s_w_folded, M, N, K, y, ldy, acc_opt, ldacc,
+                          workspace, ws_bytes, nullptr, stream);
+}
+
+extern "C" int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
+                                const void* s_star_repacked, int64_t group, const double* s_wc, int64_t M, int64_t N,
+                                int64_t K, void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace,
+                                size_t ws_bytes, cudaStream_t stream) {
+  return qqq_w4a8_gemm_ex(kModePG, aq, ldq, s_a, w_repacked, s_star_repacked, group, s_wc, M, N, K, y, ldy, acc_opt,
+                          ldacc, workspace, ws_bytes, nullptr, stream);
+}
