@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""bench.py — contract benchmark of the B200 W4A8 GEMM (QQQ, arXiv 2406.09904).
+
+Metric (BASELINE.json): "W4A8 GEMM TOPS & HBM GB/s vs M (1–1024), speedup over
+FP16 GEMM". Workload = BASELINE.json configs[1]: per-group (g=128) W4A8 GEMM,
+M sweep {1,2,4,...,1024} on the Llama-2-7B linear shapes 4096x4096,
+4096x11008, 11008x4096. One "step" = one pass over the 33 GEMMs with
+activations already quantized and resident in HBM; weights are read cold
+(rotated replicas whose total exceeds 2x the 126 MB L2).
+
+`value` = aggregate TOPS of the step (2*M*N*K summed / device time), max over
+ranks. `e2e` = the same sweep through the public API from pinned host fp16
+activations (H2D + quant_act_per_token + GEMM + D2H of y, every step).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 1024 * 1024
+SHAPES_C2 = [(4096, 4096), (4096, 11008), (11008, 4096)]
+MS_C2 = [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024]
+GROUP = 128
+METRIC = "W4A8 GEMM TOPS & HBM GB/s vs M (1-1024), speedup over FP16 GEMM"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return dict(hbm_gbs=float(pk["hbm_gbs"]), bf16_tflops=float(pk["bf16_tflops"]), source="measured")
+    except Exception:
+        return dict(hbm_gbs=6650.0, bf16_tflops=1590.0, source="fallback")
+
+
+def alg_bytes(m, k, n, scheme="per-group", g=GROUP):
+    """Algorithmic bytes per GEMM: int8 A + f64 s_A + int4 W + fp16 Y + scales."""
+    sc = 8 * n if scheme == "per-channel" else 2 * (k // g) * n + 8 * n
+    return m * k + 8 * m + k * n / 2 + 2 * m * n + sc
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_setup(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    import torch
+
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        torch.cuda.synchronize()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle = the reference algorithm restated; only here and in tests)
+# ---------------------------------------------------------------------------
+def cpu_reference_sample(seconds_budget: float = 15.0):
+    """Time the reference's own CPU path (restated in oracle/, int64 matmul split
+    over all host threads) on a bounded sample of the C2 workload."""
+    import numpy as np
+
+    from oracle import qqq_oracle as O
+
+    threads = os.cpu_count() or 1
+    k, n = SHAPES_C2[0]
+    rng = np.random.default_rng(7)
+    q4 = rng.integers(-8, 8, (k, n)).astype(np.int8)
+    s_wg = 0.02 * rng.uniform(0.5, 1.5, (k // GROUP, n))
+    qw = O.QuantizedWeights(O.pack_i4(q4), k, n, O.PER_GROUP, GROUP, s_wg=s_wg, s_wc=O.requant_scale(q4, s_wg))
+    fused = O.FusedScales.from_quantized(qw)
+    ops, t_total, points = 0.0, 0.0, []
+    for m in (1, 16):
+        x = rng.standard_normal((m, k)).astype(np.float16).astype(np.float64)
+        aq = O.quant_act_per_token(x)
+        t0 = time.perf_counter()
+        O.w4a8_gemm_per_group(aq, qw, fused, fast="threads")
+        dt = time.perf_counter() - t0
+        ops += 2.0 * m * n * k
+        t_total += dt
+        points.append(f"{k}x{n} M={m}: {dt * 1e3:.0f} ms")
+        if t_total > seconds_budget:
+            break
+    return dict(value=ops / t_total / 1e12, unit="TOPS", cores=threads, kind="port",
+                sample="per-group g=128 W4A8 GEMM (oracle restatement of gemm.py:188-203, int64 matmul over "
+                       f"{threads} host threads) on {'; '.join(points)}")
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    # one warm-up sample, then K bounded samples
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_reference_sample(5.0)
+    vals, t0 = [], time.perf_counter()
+    last = None
+    for _ in range(args.steps):
+        last = cpu_reference_sample(10.0)
+        vals.append(last["value"])
+    wall = time.perf_counter() - t0
+    v = statistics.median(vals)
+    cb = dict(last)
+    cb["value"] = v
+    line = dict(metric=METRIC, value=v, unit="TOPS", n_gpus=args.gpus, steps=args.steps, warmup=args.warmup,
+                ms_per_step=wall / max(1, args.steps) * 1e3, higher_is_better=True, scaling="weak",
+                vs_baseline=None, dtype="int8", data="synthetic",
+                config=dict(workload="C2: per-group g=128 W4A8 GEMM, M sweep 1-1024, Llama-2-7B shapes "
+                                     "(bounded CPU sample)", parallelism="host threads"),
+                impl="reference", cpu_baseline=cb,
+                e2e=dict(value=v, unit="TOPS", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def make_weights(k, n, scheme, seed, device):
+    import torch
+
+    import paper_2406_09904_b200 as Q
+    from paper_2406_09904_b200 import gemm as G
+
+    gen = torch.Generator(device=device).manual_seed(seed)
+    q4 = torch.randint(-8, 8, (k, n), dtype=torch.int8, device=device, generator=gen)
+    if scheme == "per-channel":
+        s_w = 0.02 * (0.5 + torch.rand(n, dtype=torch.float64, device=device, generator=gen))
+        qw = Q.QuantizedWeights(Q.pack_i4(q4), k, n, "per-channel", s_w=s_w)
+    else:
+        s_wg = 0.02 * (0.5 + torch.rand((k // GROUP, n), dtype=torch.float64, device=device, generator=gen))
+        qw = Q.QuantizedWeights(Q.pack_i4(q4), k, n, "per-group", GROUP, s_wg=s_wg, s_wc=Q.requant_scale(q4, s_wg))
+    fused = Q.FusedScales.from_quantized(qw)
+    return qw, fused, G.prepare(qw, fused)
+
+
+def graph_time_us(fns, reps, warm=2):
+    """Device time per launch of `fns` (captured once in a CUDA graph)."""
+    import torch
+
+    for f in fns:
+        f()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for f in fns:
+            f()
+    for _ in range(warm):
+        g.replay()
+    torch.cuda.synchronize()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) * 1e3 / (reps * len(fns))
+
+
+def run_gpu_arm(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_2406_09904_b200 as Q
+    from paper_2406_09904_b200 import gemm as G
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    peaks = load_peaks()
+    int8_peak = 2.0 * peaks["bf16_tflops"]  # dense INT8 = 2x dense bf16 (4.5 vs 2.25 PF nominal)
+    hbm_peak = peaks["hbm_gbs"]
+    shapes = SHAPES_C2
+    ms = MS_C2 if not args.quick else [1, 16, 128, 1024]
+    scheme = "per-group"
+
+    # ---- weights: one logical matrix per shape, R cold replicas ----------------
+    preps, w16 = {}, {}
+    set_bytes = sum(k * n / 2 for k, n in shapes)
+    R = max(2, math.ceil(2.5 * L2_BYTES / set_bytes))
+    for si, (k, n) in enumerate(shapes):
+        qw, fused, prep = make_weights(k, n, scheme, seed=1000 + si + 17 * rank, device=dev)
+        reps = [prep]
+        for _ in range(R - 1):
+            reps.append(G.PreparedWeights(prep.mode, prep.w.clone(), None if prep.sc is None else prep.sc.clone(),
+                                          prep.group, prep.s_col.clone()))
+        preps[(k, n)] = reps
+        w16[(k, n)] = [torch.randn((k, n), dtype=torch.float16, device=dev) for _ in range(2)]
+    acts, outs = {}, {}
+    for (k, n) in shapes:
+        for m in ms:
+            x = torch.randn((m, k), dtype=torch.float16, device=dev)
+            acts[(k, n, m)] = (x, Q.quant_act_per_token(x))
+            outs[(k, n, m)] = torch.empty((m, n), dtype=torch.float16, device=dev)
+    # pre-size the split-K workspace outside any graph capture
+    G.workspace(dev, max(Q._lib.load().qqq_gemm_workspace_bytes(max(ms), n, k) for k, n in shapes))
+
+    order = [(k, n, m) for m in ms for (k, n) in shapes]
+    counters = {s: 0 for s in shapes}
+
+    def gemm_fn(k, n, m, rep):
+        aq = acts[(k, n, m)][1]
+        y = outs[(k, n, m)]
+        p = preps[(k, n)][rep]
+        return lambda: G.run_gemm(aq, p, n, False, y_out=y)
+
+    step_fns = []
+    for (k, n, m) in order:
+        step_fns.append(gemm_fn(k, n, m, counters[(k, n)] % R))
+        counters[(k, n)] += 1
+
+    # ---- per-point device times (explanatory; not the contract number) ----------
+    points = []
+    tot_roof_t = 0.0
+    for (k, n, m) in order:
+        fns = [gemm_fn(k, n, m, r) for r in range(R)]
+        t_us = graph_time_us(fns, reps=max(2, 40 // R))
+        x = acts[(k, n, m)][0]
+        hw = w16[(k, n)]
+        f16_fns = [(lambda wi: (lambda: torch.matmul(x, wi)))(wi) for wi in hw]
+        t16 = graph_time_us(f16_fns, reps=20)
+        ops = 2.0 * m * n * k
+        byts = alg_bytes(m, k, n, scheme)
+        t_hbm = byts / (hbm_peak * 1e3)  # us
+        t_ten = ops / (int8_peak * 1e6)
+        bound = "hbm" if t_hbm >= t_ten else "tensor"
+        tot_roof_t += max(t_hbm, t_ten)
+        points.append(dict(shape=f"{k}x{n}", M=m, us=round(t_us, 3), TOPS=round(ops / t_us / 1e6, 2),
+                           GBps=round(byts / t_us / 1e3, 1), bound=bound,
+                           frac=round(max(t_hbm, t_ten) / t_us, 4), fp16_us=round(t16, 3),
+                           speedup_vs_fp16=round(t16 / t_us, 3)))
+
+    # ---- the contract timed region: K steps of the 33-GEMM sweep ---------------
+    g = torch.cuda.CUDAGraph()
+    for f in step_fns:
+        f()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        for f in step_fns:
+            f()
+    for _ in range(args.warmup):
+        g.replay()
+    barrier(world)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier(world)
+        start.record()
+        for _ in range(args.steps):
+            g.replay()
+        end.record()
+        torch.cuda.synchronize()
+        barrier(world)
+    elapsed_ms = max_over_ranks(start.elapsed_time(end), world)
+    ops_step = sum(2.0 * m * n * k for (k, n, m) in order)
+    value = sum_over_ranks(ops_step * args.steps, world) / (elapsed_ms * 1e-3) / 1e12
+    ms_per_step = elapsed_ms / args.steps
+
+    # ---- e2e through the public API from pinned host memory ---------------------
+    e2e = None
+    if not args.no_e2e:
+        host_x = {key: acts[key][0].cpu().pin_memory() for key in order}
+        host_y = {key: torch.empty(outs[key].shape, dtype=torch.float16).pin_memory() for key in order}
+        dev_x = {key: torch.empty_like(acts[key][0]) for key in order}
+        qws = {}
+        for si, (k, n) in enumerate(shapes):
+            qws[(k, n)] = make_weights(k, n, scheme, seed=1000 + si + 17 * rank, device=dev)[:2]
+
+        def e2e_step():
+            for (k, n, m) in order:
+                dx = dev_x[(k, n, m)]
+                dx.copy_(host_x[(k, n, m)], non_blocking=True)
+                aq = Q.quant_act_per_token(dx, check=False)
+                qw, fused = qws[(k, n)]
+                out = Q.w4a8_gemm_per_group(aq, qw, fused, with_acc=False)
+                host_y[(k, n, m)].copy_(out.y, non_blocking=True)
+
+        for _ in range(args.warmup):
+            e2e_step()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(time.perf_counter() - t0, world)
+        bi = sum(m * k * 2 for (k, n, m) in order)
+        bo = sum(m * n * 2 for (k, n, m) in order)
+        e2e = dict(value=sum_over_ranks(ops_step * args.steps, world) / t_e2e / 1e12, unit="TOPS",
+                   h2d_bytes_per_step=bi, d2h_bytes_per_step=bo, ms_per_step=t_e2e / args.steps * 1e3)
+
+    # ---- roofline of the dominant kernel (the W4A8 GEMM: every launch in the step)
+    step_us = ms_per_step * 1e3
+    tops = ops_step / (step_us * 1e-6) / 1e12
+    roofline = dict(bound="tensor", achieved=round(tops, 2), peak=round(int8_peak, 1), unit="TFLOP/s",
+                    frac=round(tops / int8_peak, 4), traffic=None,
+                    peak_source=f"2 x bf16_tflops of MEASURED_PEAKS.json ({peaks['source']}); dense INT8 = 2x bf16",
+                    roofline_frac_step=round(tot_roof_t / sum(p["us"] for p in points), 4),
+                    note="achieved = sum(2MNK) over the step's 33 launches / device time; per-point bounds "
+                         "(hbm below the ridge, tensor above) in roofline_points")
+    f16_total = sum(p["fp16_us"] for p in points)
+    ours_total = sum(p["us"] for p in points)
+    line = dict(metric=METRIC, value=round(value, 3), unit="TOPS", n_gpus=world, steps=args.steps,
+                warmup=args.warmup, ms_per_step=round(ms_per_step, 4), higher_is_better=True, scaling="weak",
+                vs_baseline=None, dtype="int8", data="synthetic",
+                config=dict(workload="C2 (BASELINE.json configs[1]): per-group g=128 W4A8 GEMM, M sweep "
+                                     f"{ms} x shapes {['%dx%d' % s for s in shapes]} (K x N)",
+                            scheme=scheme, group_size=GROUP, gemms_per_step=len(order),
+                            l2="weights read cold: %d rotated replicas per shape (%.0f MB > 2x L2)" % (
+                                R, R * set_bytes / 2**20),
+                            parallelism=f"replicas x{world}" if world > 1 else "single GPU"),
+                roofline=roofline,
+                fp16_baseline=dict(impl="torch.matmul fp16 (cuBLAS), same shapes, cold weights",
+                                   total_us=round(f16_total, 2), ours_total_us=round(ours_total, 2),
+                                   sweep_speedup=round(f16_total / ours_total, 3),
+                                   min_point_speedup=min(p["speedup_vs_fp16"] for p in points)),
+                roofline_points=points,
+                gpu_launches=len(order) * args.steps,
+                clocks=clk.summary())
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_reference_sample(15.0)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")), rank)
+        return
+    world, rank, local = dist_setup(args)
+    try:
+        run_gpu_arm(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -92,8 +92,12 @@ _workspaces: dict = {}
 
 
 def workspace(device: torch.device, nbytes: int) -> torch.Tensor:
-    """Zeroed split-K workspace per (device, stream); the kernels leave it zeroed."""
-    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    """Zeroed split-K workspace per device; every launch leaves it zeroed again.
+
+    GEMMs that may run concurrently on different streams must pass their own
+    workspace (run_gemm(..., ws=...)); launches on one stream share this one.
+    """
+    key = device.index
     with _ws_lock:
         ws = _workspaces.get(key)
         if ws is None or ws.numel() < nbytes:
@@ -192,7 +196,8 @@ def _aligned_q(aq: QuantizedActivations) -> torch.Tensor:
 
 
 def run_gemm(aq: QuantizedActivations, prep: PreparedWeights, n: int, with_acc: bool = True,
-             y_out: Optional[torch.Tensor] = None, cfg: Optional[dict] = None) -> GemmOutput:
+             y_out: Optional[torch.Tensor] = None, cfg: Optional[dict] = None,
+             ws: Optional[torch.Tensor] = None) -> GemmOutput:
     """Launch the W4A8 kernel on the current stream (no host sync)."""
     q = _aligned_q(aq)
     m, k = q.shape
@@ -206,7 +211,8 @@ def run_gemm(aq: QuantizedActivations, prep: PreparedWeights, n: int, with_acc: 
     if m == 0:
         return GemmOutput(y=y, acc=acc)
     wsb = lib.qqq_gemm_workspace_bytes(m, n, k)
-    ws = workspace(dev, wsb)
+    if ws is None or ws.numel() < wsb:
+        ws = workspace(dev, wsb)
     c = None
     if cfg:
         c = _lib.GemmConfig(int(cfg.get("ntok", 0)), int(cfg.get("grid", 0)), int(cfg.get("split", -1)))

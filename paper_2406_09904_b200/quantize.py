@@ -124,9 +124,10 @@ def quant_act_per_token(x, check: bool = True) -> QuantizedActivations:
     if xt.dtype not in (torch.float16, torch.float32, torch.float64):
         xt = xt.to(torch.float64)
     xt = as_cuda(xt)
-    if xt.stride(1) != 1:
-        xt = xt.contiguous()
     m, k = xt.shape
+    if xt.stride(1) != 1 or (m > 1 and xt.stride(0) < k):
+        xt = xt.contiguous()
+    ldx = xt.stride(0) if m > 1 else k
     dev = xt.device
     lib = _lib.lib_for_device(dev)
     kp = (k + 15) // 16 * 16  # 16-byte row pitch for the GEMM's TMA; view is M x K
@@ -135,7 +136,7 @@ def quant_act_per_token(x, check: bool = True) -> QuantizedActivations:
     status = _status(dev)
     if m > 0 and k > 0:
         dt = {torch.float16: 0, torch.float32: 1, torch.float64: 2}[xt.dtype]
-        _lib.check(lib.qqq_act_quant(_lib.ptr(xt), dt, m, k, xt.stride(0), _lib.ptr(qbuf), kp, _lib.ptr(s_a),
+        _lib.check(lib.qqq_act_quant(_lib.ptr(xt), dt, m, k, ldx, _lib.ptr(qbuf), kp, _lib.ptr(s_a),
                                      _lib.ptr(status), _lib.stream_of(dev)), "quant_act_per_token")
     elif k == 0:
         raise ShapeError("activations must have K >= 1")
