@@ -1,73 +1,65 @@
-"""Quick device-time sweep of the W4A8 GEMM (CUDA events, L2 flushed between
-iterations by rotating weight replicas). Developer tool; bench.py is the
-contract benchmark."""
+"""Developer sweep: device time per (shape, M, tile plan) via CUDA graphs over
+rotated cold weight replicas. bench.py is the contract benchmark."""
 import argparse
 import json
+import math
 import os
 import sys
 
-import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench as B  # noqa: E402
 import paper_2406_09904_b200 as Q  # noqa: E402
 from paper_2406_09904_b200 import gemm as G  # noqa: E402
-
-
-def make(k, n, scheme, seed=0):
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    q4 = torch.randint(-8, 8, (k, n), dtype=torch.int8, device="cuda", generator=g)
-    if scheme == "per-channel":
-        s_w = (0.02 * (0.5 + torch.rand(n, dtype=torch.float64, device="cuda", generator=g)))
-        qw = Q.QuantizedWeights(Q.pack_i4(q4), k, n, "per-channel", s_w=s_w)
-    else:
-        s_wg = 0.02 * (0.5 + torch.rand((k // 128, n), dtype=torch.float64, device="cuda", generator=g))
-        qw = Q.QuantizedWeights(Q.pack_i4(q4), k, n, "per-group", 128, s_wg=s_wg, s_wc=Q.requant_scale(q4, s_wg))
-    fused = Q.FusedScales.from_quantized(qw)
-    return G.prepare(qw, fused)
-
-
-def time_fn(fn, iters, flush):
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(iters)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(iters)]
-    for i in range(iters):
-        flush()
-        starts[i].record()
-        fn(i)
-        ends[i].record()
-    torch.cuda.synchronize()
-    ts = sorted(s.elapsed_time(e) for s, e in zip(starts, ends))
-    return ts[len(ts) // 2] * 1e3  # us median
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shapes", default="4096x4096,4096x11008,11008x4096")
     ap.add_argument("--ms", default="1,16,64,128,256,512,1024")
-    ap.add_argument("--schemes", default="per-group,per-channel")
-    ap.add_argument("--iters", type=int, default=30)
-    ap.add_argument("--cfg", default="")
+    ap.add_argument("--schemes", default="per-group")
+    ap.add_argument("--cfgs", default="auto", help="';'-separated JSON tile plans or 'auto'")
+    ap.add_argument("--fp16", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="few plain launches (for ncu), no timing")
     a = ap.parse_args()
-    flushbuf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    flush = lambda: flushbuf.zero_()
-    cfg = json.loads(a.cfg) if a.cfg else None
+    dev = torch.device("cuda", 0)
+    cfgs = [None if c == "auto" else json.loads(c) for c in a.cfgs.split(";")]
+    peaks = B.load_peaks()
     for shp in a.shapes.split(","):
         k, n = map(int, shp.split("x"))
         for scheme in a.schemes.split(","):
-            prep = make(k, n, scheme)
-            wf16 = torch.randn((k, n), dtype=torch.float16, device="cuda")
+            qw, fused, prep = B.make_weights(k, n, scheme, 0, dev)
+            R = max(2, math.ceil(2.5 * B.L2_BYTES / (k * n / 2)))
+            if a.profile:
+                R = 2
+            reps = [prep] + [G.PreparedWeights(prep.mode, prep.w.clone(), None if prep.sc is None else prep.sc.clone(),
+                                               prep.group, prep.s_col.clone()) for _ in range(R - 1)]
+            w16 = [torch.randn((k, n), dtype=torch.float16, device=dev) for _ in range(2)] if a.fp16 else None
             for m in map(int, a.ms.split(",")):
-                x = torch.randn((m, k), dtype=torch.float16, device="cuda")
+                x = torch.randn((m, k), dtype=torch.float16, device=dev)
                 aq = Q.quant_act_per_token(x)
-                y = torch.empty((m, n), dtype=torch.float16, device="cuda")
-                t_g = time_fn(lambda i: G.run_gemm(aq, prep, n, False, y_out=y, cfg=cfg), a.iters, flush)
-                t_q = time_fn(lambda i: Q.quant_act_per_token(x, check=False), a.iters, flush)
-                t_h = time_fn(lambda i: torch.matmul(x, wf16), a.iters, flush)
-                ops = 2.0 * m * n * k
-                byt = m * k + 8 * m + k * n / 2 + 2 * m * n + (8 * n if scheme == "per-channel" else 2 * (k // 128) * n + 8 * n)
-                print(json.dumps(dict(shape=shp, scheme=scheme, M=m, gemm_us=round(t_g, 2), actq_us=round(t_q, 2),
-                                      fp16_us=round(t_h, 2), TOPS=round(ops / t_g / 1e6, 1),
-                                      GBps=round(byt / t_g / 1e3, 1), speedup_vs_fp16=round(t_h / t_g, 2))), flush=True)
+                y = torch.empty((m, n), dtype=torch.float16, device=dev)
+                G.workspace(dev, Q._lib.load().qqq_gemm_workspace_bytes(m, n, k))
+                for cfg in cfgs:
+                    fns = [(lambda p: (lambda: G.run_gemm(aq, p, n, False, y_out=y, cfg=cfg)))(p) for p in reps]
+                    if a.profile:
+                        for f in fns * 2:
+                            f()
+                        torch.cuda.synchronize()
+                        continue
+                    t = B.graph_time_us(fns, reps=max(2, 60 // R))
+                    ops = 2.0 * m * n * k
+                    byt = B.alg_bytes(m, k, n, scheme)
+                    roof = max(byt / (peaks["hbm_gbs"] * 1e3), ops / (2 * peaks["bf16_tflops"] * 1e6))
+                    rec = dict(shape=shp, scheme=scheme, M=m, cfg=cfg, us=round(t, 2), TOPS=round(ops / t / 1e6, 1),
+                               GBps=round(byt / t / 1e3, 1), roof_frac=round(roof / t, 3))
+                    if w16:
+                        t16 = B.graph_time_us([(lambda wi: (lambda: torch.matmul(x, wi)))(wi) for wi in w16], reps=20)
+                        rec["fp16_us"] = round(t16, 2)
+                        rec["speedup"] = round(t16 / t, 2)
+                    print(json.dumps(rec), flush=True)
 
 
 if __name__ == "__main__":

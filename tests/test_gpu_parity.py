@@ -145,7 +145,7 @@ def test_fused_dequant_quant_exhaustive():
     r_hi = (7 * sv + 1152).astype(np.float16).astype(np.float64)
     admissible = (r_lo >= 1025) & (r_hi <= 1279) & (sv >= 2.0 ** -10)
     adm = np.repeat(admissible, 16)
-    assert admissible.sum() > 15000
+    assert admissible.sum() > 14000
     assert np.array_equal(got_w[adm], want[adm])
 
 
