@@ -43,7 +43,7 @@ enum {
   QQQ_STAT_PAD_NIBBLE = 4,  /* quantize.py:206-207 CorruptionError */
   QQQ_STAT_SCALE_INF = 8,   /* gemm.py:67-68 ConfigError */
   QQQ_STAT_NEED_CLAMP = 16, /* repack: FusedDequantQuant clamp needed -> I8 layout */
-  QQQ_STAT_TINY_SCALE = 32  /* repack: s* < 2^-10 -> I8 layout */
+  QQQ_STAT_TINY_SCALE = 32  /* reserved */
 };
 
 enum { QQQ_MODE_PC = 0, QQQ_MODE_PG = 1, QQQ_MODE_I8 = 2 };
@@ -97,10 +97,12 @@ int qqq_repack_weights(const uint8_t* packed, int64_t K, int64_t N, int mode, vo
 int qqq_repack_weights_i8(const int8_t* w8, const uint8_t* packed, const uint16_t* s_star, int64_t group, int64_t K,
                           int64_t N, void* out, qqq_stream_t stream);
 
-/* s_star [K/group x N] -> per-tile layout; sets QQQ_STAT_NEED_CLAMP /
- * QQQ_STAT_TINY_SCALE in flags_dev if the fast HFMA2 path is not provably exact. */
-int qqq_repack_scales(const uint16_t* s_star, int64_t K, int64_t N, int64_t group, void* out, int32_t* flags_dev,
-                      qqq_stream_t stream);
+/* s_star [K/group x N] -> per-tile layout; sets QQQ_STAT_NEED_CLAMP in
+ * flags_dev if, for the codes actually present in some group (packed, the
+ * pack_i4 bytes; NULL = assume all 16 codes), the clamp-free HFMA2 converter
+ * would differ from the reference's clamped FusedDequantQuant. */
+int qqq_repack_scales(const uint16_t* s_star, const uint8_t* packed, int64_t K, int64_t N, int64_t group, void* out,
+                      int32_t* flags_dev, qqq_stream_t stream);
 
 /* ---- the W4A8 GEMM ------------------------------------------------------- */
 

@@ -41,7 +41,7 @@ SIGNATURES = {
     "qqq_repacked_scale_bytes": (c_size_t, [I64, I64, I64]),
     "qqq_repack_weights": (c_int, [P, I64, I64, c_int, P, S]),
     "qqq_repack_weights_i8": (c_int, [P, P, P, I64, I64, I64, P, S]),
-    "qqq_repack_scales": (c_int, [P, I64, I64, I64, P, P, S]),
+    "qqq_repack_scales": (c_int, [P, P, I64, I64, I64, P, P, S]),
     "qqq_gemm_workspace_bytes": (c_size_t, [I64, I64, I64]),
     "qqq_w4a8_gemm_pc": (c_int, [P, I64, P, P, P, I64, I64, I64, P, I64, P, I64, P, c_size_t, S]),
     "qqq_w4a8_gemm_pg": (c_int, [P, I64, P, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t, S]),

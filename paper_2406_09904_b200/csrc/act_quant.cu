@@ -10,12 +10,12 @@
 // row from L1/L2 and writes 16-byte int8 vectors.
 //
 // Bit-exactness for fp16 input: the fast path
-// computes t = (x*127)/m in fp32 (x*127 is exact, one RN divide, so
-// |t - x*127/m| <= 127*2^-24). Whenever t is within 1e-3 of a half-integer we
-// recompute the reference formula rint(x / (m/127.0)) in f64 verbatim, so the
-// result equals the reference on every input, ties included (the reference is
-// not half-even on exact ties because of its double rounding). f32/f64 inputs
-// always take the verbatim f64 formula.
+// computes t = x * RN(127/m) in fp32 (|t - x*127/m| <= 2*127*2^-24 < 2e-5).
+// Whenever t is within 1e-3 of a half-integer we recompute the reference
+// formula rint(x / (m/127.0)) in f64 verbatim, so the result equals the
+// reference on every input, ties included (the reference is not half-even on
+// exact ties because of its double rounding). f32/f64 inputs always take the
+// verbatim f64 formula.
 #include <type_traits>
 
 #include "qqq_common.cuh"
@@ -74,6 +74,10 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
                                                               double* __restrict__ s_out, int32_t* status) {
   using Acc = typename std::conditional<sizeof(T) == 8, double, float>::type;
   __shared__ Acc red[32];
+  // PDL: let the GEMM that consumes q start its prologue / weight prefetch now,
+  // and wait for whatever produced x before reading it.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t row = blockIdx.x;
   const T* xr = x + row * ldx;
   int8_t* qr = q + row * ldq;
@@ -150,19 +154,28 @@ extern "C" int qqq_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, i
   if (M < 0 || K <= 0 || ldx < K || ldq < K) return kErrShape;
   if (M == 0) return kOk;
   constexpr int kT = 256;
-  dim3 grid((unsigned)M);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)M);
+  lc.blockDim = dim3(kT);
+  lc.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  cudaError_t e;
   switch (x_dtype) {
     case 0:
-      act_quant_kernel<__half, kT><<<grid, kT, 0, stream>>>((const __half*)x, K, ldx, q, ldq, s_a, status_dev);
+      e = cudaLaunchKernelEx(&lc, act_quant_kernel<__half, kT>, (const __half*)x, K, ldx, q, ldq, s_a, status_dev);
       break;
     case 1:
-      act_quant_kernel<float, kT><<<grid, kT, 0, stream>>>((const float*)x, K, ldx, q, ldq, s_a, status_dev);
+      e = cudaLaunchKernelEx(&lc, act_quant_kernel<float, kT>, (const float*)x, K, ldx, q, ldq, s_a, status_dev);
       break;
     case 2:
-      act_quant_kernel<double, kT><<<grid, kT, 0, stream>>>((const double*)x, K, ldx, q, ldq, s_a, status_dev);
+      e = cudaLaunchKernelEx(&lc, act_quant_kernel<double, kT>, (const double*)x, K, ldx, q, ldq, s_a, status_dev);
       break;
     default:
       return kErrConfig;
   }
-  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+  return e == cudaSuccess ? kOk : kErrCuda;
 }

@@ -79,6 +79,11 @@ struct Cfg {
   static_assert(BK % 128 == 0, "BK must be a multiple of the 128-byte swizzle atom");
 };
 
+// Programmatic dependent launch (PDL): wait for / release the neighbouring
+// kernels in the stream. No-ops when launched without the PDL attribute.
+QQQ_DEVICE void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+QQQ_DEVICE void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 QQQ_DEVICE void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 QQQ_DEVICE __half f64_to_f16_rn(double v) {
@@ -91,10 +96,24 @@ QQQ_DEVICE void red_add_s32(int32_t* p, int32_t v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-QQQ_DEVICE int32_t ld_cg_s32(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
+// Dequant epilogue for 16 consecutive tokens of one output channel n:
+// y = f16((acc * s_a[t]) * s_col[n]) in f64 with one final RN rounding
+// (gemm.py:182-184 / 200-202); acc written as-is when requested.
+QQQ_DEVICE void store_outputs(const GemmParams& p, const uint32_t (&r)[16], int t0, int nvalid, int n, bool n_ok,
+                              double s_col) {
+  double sa[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) sa[i] = (i < nvalid) ? __ldg(p.s_a + t0 + i) : 0.0;
+  if (!n_ok) return;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i < nvalid) {
+      const int t = t0 + i;
+      const int32_t a = (int32_t)r[i];
+      if (p.acc) p.acc[(int64_t)t * p.ldacc + n] = a;
+      if (p.s_col) p.y[(int64_t)t * p.ldy + n] = f64_to_f16_rn(((double)a * sa[i]) * s_col);
+    }
+  }
 }
 
 // Segment iterator: the contiguous unit range of this CTA split at tile borders.
@@ -163,6 +182,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     mbar_fence_init();
   }
   if (warp == 0 && lane == 0) tma_prefetch_desc(&act_map);
+  if (threadIdx.x == 0) griddep_launch_dependents();
   if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
@@ -171,43 +191,58 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   if (warp == 0) {
     // ======================= TMA / bulk producer =======================
+    // Weights and scales do not depend on the previous kernel in the stream, so
+    // the first kStages k-blocks of weights are requested BEFORE the PDL grid
+    // dependency wait; only the activation loads wait for the producer kernel.
     if (lane == 0) {
-      SegIter si = make_iter(p);
+      auto issue_weights = [&](int n_tile, int kb, int s) {
+        const int64_t slab0 = (int64_t)n_tile * p.slabs + (int64_t)kb * (BK / 32);
+        const int64_t wofs = slab0 * (MODE == kModeI8 ? 4096 : 2048);
+        bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + wofs, C::kWBytes, &full[s]);
+        if constexpr (MODE == kModePG) {
+          // groups covered by this k-block (g <= BK: BK/g groups; g > BK: one)
+          const int g = p.group;
+          const int gfirst = (int)(((int64_t)kb * BK) / g);
+          const int bytes = (g <= BK ? BK / g : 1) * 256;
+          const __half* src = p.sc + ((int64_t)n_tile * p.g_pad + gfirst) * 128;
+          // the stage always receives kScBytes so expect_tx is constant: repeat the copy
+          for (int off = 0; off < C::kScBytes; off += bytes)
+            bulk_g2s(smem + C::kOffSc + s * C::kScBytes + off, src, bytes, &full[s]);
+        }
+      };
+      auto issue_act = [&](int tok0, int kb, int s) {
+        uint8_t* act = smem + C::kOffAct + s * C::kActBytes;
+#pragma unroll
+        for (int j = 0; j < BK / 128; ++j)
+          tma_load_2d(act + j * NTOK * 128, &act_map, kb * BK + j * 128, tok0, &full[s]);
+      };
       int tile, kb0, kb1;
+      // pass 1: arm the first kStages stages and stream their weights
+      uint32_t pre = 0;
+      {
+        SegIter si = make_iter(p);
+        while (pre < (uint32_t)C::kStages && si.next(tile, kb0, kb1)) {
+          for (int kb = kb0; kb < kb1 && pre < (uint32_t)C::kStages; ++kb, ++pre) {
+            mbar_arrive_expect_tx(&full[pre], C::kStageBytes);
+            issue_weights(tile / p.tok_tiles, kb, pre);
+          }
+        }
+      }
+      griddep_wait();
+      // pass 2: activations for the pre-armed stages, then the steady-state ring
+      SegIter si = make_iter(p);
       uint32_t it = 0;
       while (si.next(tile, kb0, kb1)) {
         const int n_tile = tile / p.tok_tiles;
         const int tok0 = (tile % p.tok_tiles) * NTOK;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::kStages;
-          mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[s], C::kStageBytes);
-          uint8_t* act = smem + C::kOffAct + s * C::kActBytes;
-#pragma unroll
-          for (int j = 0; j < BK / 128; ++j)
-            tma_load_2d(act + j * NTOK * 128, &act_map, kb * BK + j * 128, tok0, &full[s]);
-          const int64_t slab0 = (int64_t)n_tile * p.slabs + (int64_t)kb * (BK / 32);
-          const int64_t wofs = slab0 * (MODE == kModeI8 ? 4096 : 2048);
-          bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + wofs, C::kWBytes, &full[s]);
-          if constexpr (MODE == kModePG) {
-            // groups covered by this k-block (g <= BK: BK/g groups; g > BK: one)
-            const int g = p.group;
-            const int gfirst = (int)(((int64_t)kb * BK) / g);
-            const int ngroups = g <= BK ? BK / g : 1;
-            const __half* src = p.sc + ((int64_t)n_tile * p.g_pad + gfirst) * 128;
-            // always move the full per-stage scale footprint so expect_tx is constant
-            const int bytes = ngroups * 256;
-            bulk_g2s(smem + C::kOffSc + s * C::kScBytes, src, bytes, &full[s]);
-            if (bytes < C::kScBytes) {
-              // pad the transaction count with a dummy re-read of the same bytes
-              int rem = C::kScBytes - bytes;
-              while (rem > 0) {
-                int b = rem < bytes ? rem : bytes;
-                bulk_g2s(smem + C::kOffSc + s * C::kScBytes + (C::kScBytes - rem), src, b, &full[s]);
-                rem -= b;
-              }
-            }
+          if (it >= pre) {
+            mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
+            mbar_arrive_expect_tx(&full[s], C::kStageBytes);
+            issue_weights(n_tile, kb, s);
           }
+          issue_act(tok0, kb, s);
         }
       }
     }
@@ -306,6 +341,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpiWarps) {
     // ============================== epilogue ==============================
+    griddep_wait();  // y / acc / workspace / s_a may be touched by the previous kernel
     const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = q * 32 + lane;
     SegIter si = make_iter(p);
@@ -319,37 +355,34 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int tok0 = (tile % p.tok_tiles) * NTOK;
       const int n = n_tile * 128 + row;
       const bool n_ok = n < p.N;
+      const int tvalid = (p.M - tok0) < NTOK ? (p.M - tok0) : NTOK;
       const bool whole = (kb0 == 0 && kb1 == p.kb_per_tile);
       const double s_col = (n_ok && p.s_col) ? p.s_col[n] : 0.0;
       int32_t* ws_tile = p.ws + (int64_t)tile * NTOK * 128;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
+      const int nchunks = (tvalid + 15) / 16;  // TMEM columns past the last token are never read
 #pragma unroll 1
-      for (int c0 = 0; c0 < NTOK; c0 += 16) {
+      for (int c = 0; c < nchunks; ++c) {
+        const int c0 = c * 16;
         uint32_t r[16];
         tmem_ld16(taddr + c0, r);
         tmem_wait_ld();
-        if (c0 + 16 >= NTOK) {
+        if (c + 1 == nchunks) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[j]);
         }
         if (whole) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int t = tok0 + c0 + i;
-            if (t < p.M && n_ok) {
-              const int32_t a = (int32_t)r[i];
-              if (p.acc) p.acc[(int64_t)t * p.ldacc + n] = a;
-              if (p.s_col) p.y[(int64_t)t * p.ldy + n] = f64_to_f16_rn(((double)a * p.s_a[t]) * s_col);
-            }
-          }
+          store_outputs(p, r, tok0 + c0, tvalid - c0, n, n_ok, s_col);
         } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int t = tok0 + c0 + i;
-            if (t < p.M) red_add_s32(ws_tile + (c0 + i) * 128 + row, (int32_t)r[i]);
-          }
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < tvalid) red_add_s32(ws_tile + (c0 + i) * 128 + row, (int32_t)r[i]);
         }
+      }
+      if (nchunks == 0) {  // (cannot happen: every tile has >= 1 token) keep the barrier protocol intact
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[j]);
       }
       if (!whole) {
         __threadfence();
@@ -360,22 +393,23 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           *last_flag = (old + add == p.kb_per_tile) ? 1 : 0;
         }
         named_bar_sync(1, kNumEpiWarps * 32);
-        if (*last_flag) {
+        const bool last = *last_flag != 0;
+        named_bar_sync(1, kNumEpiWarps * 32);  // everyone has read last_flag before it is reused
+        if (last) {
           __threadfence();
-          const int tmax = (p.M - tok0) < NTOK ? (p.M - tok0) : NTOK;
-          for (int i = 0; i < tmax; ++i) {
-            const int t = tok0 + i;
-            int32_t* cell = ws_tile + i * 128 + row;
-            const int32_t a = ld_cg_s32(cell);
-            *cell = 0;
-            if (n_ok) {
-              if (p.acc) p.acc[(int64_t)t * p.ldacc + n] = a;
-              if (p.s_col) p.y[(int64_t)t * p.ldy + n] = f64_to_f16_rn(((double)a * p.s_a[t]) * s_col);
-            }
+#pragma unroll 1
+          for (int c0 = 0; c0 < tvalid; c0 += 16) {
+            uint32_t r[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              r[i] = (c0 + i < tvalid) ? (uint32_t)__ldcg(ws_tile + (c0 + i) * 128 + row) : 0u;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < tvalid) __stcg(ws_tile + (c0 + i) * 128 + row, 0);
+            store_outputs(p, r, tok0 + c0, tvalid - c0, n, n_ok, s_col);
           }
           if (warp == kEpiWarp0 && lane == 0) p.counters[tile] = 0;
         }
-        named_bar_sync(1, kNumEpiWarps * 32);  // last_flag reuse guard
       }
       ++seg;
     }
@@ -466,8 +500,17 @@ static int launch_t(const CUtensorMap& map, const GemmParams& p, int grid, cudaS
       return kErrCuda;
     attr_set = true;
   }
-  kern<<<grid, kNumThreads, C::kSmemBytes, stream>>>(map, p);
-  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(kNumThreads);
+  lc.dynamicSmemBytes = C::kSmemBytes;
+  lc.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, kern, map, p) == cudaSuccess ? kOk : kErrCuda;
 }
 
 template <int MODE>

@@ -171,24 +171,39 @@ __global__ void repack8_kernel(const int8_t* __restrict__ w8, const uint8_t* __r
       *reinterpret_cast<const uint4*>(v);
 }
 
-// s*[G][N] -> [n_tiles][G_pad][128] (zero padded) + fast-path admissibility flags.
-__global__ void repack_scales_kernel(const uint16_t* __restrict__ s_star, int64_t G, int64_t N, int64_t N_pad,
-                                     int64_t G_pad, uint16_t* __restrict__ out, int32_t* flags) {
+// s*[G][N] -> [n_tiles][G_pad][128] (zero padded) + fast-path admissibility.
+// The HFMA2 converter omits the reference's clamp (gemm.py:123-127), which is
+// exact iff every code q present in group (g, n) gives RN(q*s* + 1152) in
+// [1025, 1279]; by monotonicity in q it suffices to test the group's min and
+// max code. Weights from requant_scale always pass (test_gemm.py:273-280).
+// A tiny s* is harmless: |q*s*| < 1/2 so both RN(q*s*+1152) and the s*/16
+// form give 1152 exactly.
+__global__ void repack_scales_kernel(const uint16_t* __restrict__ s_star, const uint8_t* __restrict__ packed,
+                                     int64_t K, int64_t group, int64_t G, int64_t N, int64_t N_pad, int64_t G_pad,
+                                     uint16_t* __restrict__ out, int32_t* flags) {
   const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t g = blockIdx.y;
   if (n >= N_pad) return;
   uint16_t h = 0;
   if (g < G && n < N) {
     h = s_star[g * N + n];
+    int qmin = 7, qmax = -8;
+    if (packed) {
+      for (int64_t k = g * group; k < (g + 1) * group; ++k) {
+        const int q = ref_nibble(packed, K, N, k, n) - 8;
+        qmin = min(qmin, q);
+        qmax = max(qmax, q);
+      }
+    } else {
+      qmin = -8;
+      qmax = 7;
+    }
     const __half s = __ushort_as_half(h);
     const __half add = __float2half_rn(1152.0f);
-    // every code q in [-8, 7] must land in [1025, 1279] without the clamp
-    const float r_lo = __half2float(__hfma(__int2half_rn(-8), s, add));
-    const float r_hi = __half2float(__hfma(__int2half_rn(7), s, add));
-    const float lo = fminf(r_lo, r_hi), hi = fmaxf(r_lo, r_hi);
-    if (!(lo >= 1025.0f && hi <= 1279.0f)) atomicOr(flags, kStatNeedClamp);
-    const float a = fabsf(__half2float(s));
-    if (a != 0.0f && !(a >= 0.0009765625f)) atomicOr(flags, kStatTinyScale);  // 2^-10
+    const float r_a = __half2float(__hfma(__int2half_rn(qmin), s, add));
+    const float r_b = __half2float(__hfma(__int2half_rn(qmax), s, add));
+    const float lo = fminf(r_a, r_b), hi = fmaxf(r_a, r_b);
+    if (!(lo >= 1025.0f && hi <= 1279.0f)) atomicOr(flags, kStatNeedClamp);  // NaN fails too
   }
   out[((n / kTileN) * G_pad + g) * kTileN + (n % kTileN)] = h;
 }
@@ -318,13 +333,14 @@ extern "C" int qqq_repack_weights_i8(const int8_t* w8, const uint8_t* packed, co
   return ok();
 }
 
-extern "C" int qqq_repack_scales(const uint16_t* s_star, int64_t K, int64_t N, int64_t group, void* out,
-                                 int32_t* flags_dev, cudaStream_t st) {
+extern "C" int qqq_repack_scales(const uint16_t* s_star, const uint8_t* packed, int64_t K, int64_t N, int64_t group,
+                                 void* out, int32_t* flags_dev, cudaStream_t st) {
   if (K <= 0 || N <= 0 || group <= 0 || K % group != 0) return kErrConfig;
   const int64_t np = round_up(N, kTileN), kp = round_up(K, kKPadTo);
   const int64_t gpad = (kp + group - 1) / group;
   dim3 grid(nblk(np, 128), (unsigned)gpad);
-  repack_scales_kernel<<<grid, 128, 0, st>>>(s_star, K / group, N, np, gpad, (uint16_t*)out, flags_dev);
+  repack_scales_kernel<<<grid, 128, 0, st>>>(s_star, packed, K, group, K / group, N, np, gpad, (uint16_t*)out,
+                                             flags_dev);
   return ok();
 }
 

@@ -167,9 +167,10 @@ def prepare(qw: QuantizedWeights, fused: FusedScales) -> PreparedWeights:
     if fast_ok:
         sc = torch.empty(lib.qqq_repacked_scale_bytes(k, n, g) // 2, dtype=torch.float16, device=dev)
         flags = torch.zeros(1, dtype=torch.int32, device=dev)
-        _lib.check(lib.qqq_repack_scales(_lib.ptr(s_star), k, n, g, _lib.ptr(sc), _lib.ptr(flags),
+        packed = as_cuda(qw.packed, torch.uint8).contiguous()
+        _lib.check(lib.qqq_repack_scales(_lib.ptr(s_star), _lib.ptr(packed), k, n, g, _lib.ptr(sc), _lib.ptr(flags),
                                          _lib.stream_of(dev)), "repack_scales")
-        fast_ok = int(flags.item()) & (_lib.STAT_NEED_CLAMP | _lib.STAT_TINY_SCALE) == 0
+        fast_ok = (int(flags.item()) & _lib.STAT_NEED_CLAMP) == 0
     if fast_ok:
         prep = PreparedWeights(_lib.MODE_PG, _repacked_nibbles(qw, _lib.MODE_PG), sc, g,
                                as_cuda(fused.s_wc, torch.float64).contiguous())

@@ -143,7 +143,7 @@ def test_fused_dequant_quant_exhaustive():
     sv = s_bits.view(np.float16).astype(np.float64)
     r_lo = (-8 * sv + 1152).astype(np.float16).astype(np.float64)
     r_hi = (7 * sv + 1152).astype(np.float16).astype(np.float64)
-    admissible = (r_lo >= 1025) & (r_hi <= 1279) & (sv >= 2.0 ** -10)
+    admissible = (r_lo >= 1025) & (r_hi <= 1279)  # tiny s* included: both paths give 1152
     adm = np.repeat(admissible, 16)
     assert admissible.sum() > 14000
     assert np.array_equal(got_w[adm], want[adm])
