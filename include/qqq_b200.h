@@ -129,6 +129,7 @@ typedef struct qqq_gemm_config {
   int ntok;  /* tokens per UMMA tile: 16/32/64/128/256, 0 = auto */
   int grid;  /* CTAs for stream-K, 0 = auto */
   int split; /* -1 auto, 0 whole tiles, 1 stream-K */
+  void* dbg; /* optional device buffer [grid][64] u64: per-CTA %globaltimer timeline (diagnostics) */
 } qqq_gemm_config;
 
 int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,

@@ -21,7 +21,7 @@ MODE_PC, MODE_PG, MODE_I8 = 0, 1, 2
 
 
 class GemmConfig(ctypes.Structure):
-    _fields_ = [("ntok", c_int), ("grid", c_int), ("split", c_int)]
+    _fields_ = [("ntok", c_int), ("grid", c_int), ("split", c_int), ("dbg", c_void_p)]
 
 
 P = c_void_p

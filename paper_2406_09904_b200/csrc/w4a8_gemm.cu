@@ -51,7 +51,19 @@ struct GemmParams {
   int n_tiles, tok_tiles, kb_per_tile, slabs, g_pad, group;
   int64_t units;
   int aligned_tiles;  // >0: CTA b owns whole tiles [b*aligned_tiles, ...)
+  unsigned long long* dbg;  // optional per-CTA timeline (kDbgSlots %globaltimer stamps), diagnostics only
 };
+
+constexpr int kDbgSlots = 64;
+QQQ_DEVICE unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define QQQ_STAMP(slot)                                                          \
+  do {                                                                           \
+    if (p.dbg) p.dbg[(size_t)blockIdx.x * kDbgSlots + (slot)] = gtimer();        \
+  } while (0)
 
 template <int MODE, int NTOK, int BK>
 struct Cfg {
@@ -166,6 +178,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
+  if (threadIdx.x == 0) QQQ_STAMP(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -188,6 +201,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) QQQ_STAMP(1);
 
   if (warp == 0) {
     // ======================= TMA / bulk producer =======================
@@ -228,7 +242,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
         }
       }
+      QQQ_STAMP(2);
       griddep_wait();
+      QQQ_STAMP(3);
       // pass 2: activations for the pre-armed stages, then the steady-state ring
       SegIter si = make_iter(p);
       uint32_t it = 0;
@@ -281,6 +297,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             mma_i8_ss(d_tmem, a_desc, b_desc, C::kIdesc, (kb > kb0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&empty[s]);
+          if (it < 16) QQQ_STAMP(20 + it);
           if constexpr (C::kConvert) {
             mma_commit(&a_empty[b]);
             ++ait;
@@ -301,6 +318,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb, ++it, ++ait) {
           const int s = it % C::kStages;
           mbar_wait(&full[s], (it / C::kStages) & 1);
+          if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(4 + it);
           const int b = ait % C::kABufs;
           mbar_wait(&a_empty[b], ((ait / C::kABufs) & 1) ^ 1);
           const uint8_t* wst = smem + C::kOffW + s * C::kWBytes;
@@ -351,6 +369,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int j = seg & 1;
       mbar_wait(&acc_full[j], (seg >> 1) & 1);
       tc_fence_after();
+      if (threadIdx.x == kEpiWarp0 * 32 && seg < 4) QQQ_STAMP(36 + 2 * seg);
       const int n_tile = tile / p.tok_tiles;
       const int tok0 = (tile % p.tok_tiles) * NTOK;
       const int n = n_tile * 128 + row;
@@ -411,11 +430,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           if (warp == kEpiWarp0 && lane == 0) p.counters[tile] = 0;
         }
       }
+      if (threadIdx.x == kEpiWarp0 * 32 && seg < 4) QQQ_STAMP(37 + 2 * seg);
       ++seg;
     }
   }
 
   __syncthreads();
+  if (threadIdx.x == 0) QQQ_STAMP(63);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);
@@ -594,6 +615,7 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   p.g_pad = group > 0 ? (int)((round_up(K, kKPadTo) + group - 1) / group) : 0;
   p.units = lp.units;
   p.aligned_tiles = lp.aligned_tiles;
+  p.dbg = cfg ? (unsigned long long*)cfg->dbg : nullptr;
 
   switch (mode) {
     case kModePC: return launch_mode<kModePC>(lp.ntok, map, p, lp.grid, stream);

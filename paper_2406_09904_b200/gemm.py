@@ -216,7 +216,9 @@ def run_gemm(aq: QuantizedActivations, prep: PreparedWeights, n: int, with_acc: 
         ws = workspace(dev, wsb)
     c = None
     if cfg:
-        c = _lib.GemmConfig(int(cfg.get("ntok", 0)), int(cfg.get("grid", 0)), int(cfg.get("split", -1)))
+        dbg = cfg.get("dbg")
+        c = _lib.GemmConfig(int(cfg.get("ntok", 0)), int(cfg.get("grid", 0)), int(cfg.get("split", -1)),
+                            None if dbg is None else dbg.data_ptr())
     rc = lib.qqq_w4a8_gemm_ex(prep.mode, _lib.ptr(q), q.stride(0), _lib.ptr(s_a), _lib.ptr(prep.w),
                               _lib.ptr(prep.sc), prep.group, _lib.ptr(prep.s_col), m, n, k, _lib.ptr(y), y.stride(0),
                               _lib.ptr(acc), n, _lib.ptr(ws), ws.numel(),

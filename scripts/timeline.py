@@ -1,0 +1,50 @@
+"""Per-CTA in-kernel timeline (%globaltimer stamps) of one W4A8 GEMM launch."""
+import argparse, json, os, sys
+import numpy as np
+import torch
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench as B
+import paper_2406_09904_b200 as Q
+from paper_2406_09904_b200 import gemm as G
+
+NAMES = {0: "start", 1: "setup", 2: "w_issued", 3: "dep_wait", 63: "end"}
+for i in range(16):
+    NAMES[4 + i] = f"full{i}"
+    NAMES[20 + i] = f"mma{i}"
+for sg in range(4):
+    NAMES[36 + 2 * sg] = f"accfull{sg}"
+    NAMES[37 + 2 * sg] = f"epi_done{sg}"
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--shape", default="4096x11008")
+ap.add_argument("--m", type=int, default=16)
+ap.add_argument("--scheme", default="per-group")
+ap.add_argument("--cfg", default="{}")
+a = ap.parse_args()
+k, n = map(int, a.shape.split("x"))
+dev = torch.device("cuda", 0)
+qw, fused, prep = B.make_weights(k, n, a.scheme, 0, dev)
+x = torch.randn((a.m, k), dtype=torch.float16, device=dev)
+aq = Q.quant_act_per_token(x)
+y = torch.empty((a.m, n), dtype=torch.float16, device=dev)
+flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+for rep in range(3):
+    dbg = torch.zeros((1024, 64), dtype=torch.int64, device=dev)
+    cfg = dict(json.loads(a.cfg), dbg=dbg)
+    flush.zero_()
+    torch.cuda.synchronize()
+    G.run_gemm(aq, prep, n, False, y_out=y, cfg=cfg)
+    torch.cuda.synchronize()
+d = dbg.cpu().numpy().astype(np.int64)
+ctas = d[:, 0] > 0
+d = d[ctas]
+t0 = d[:, 0].min()
+print(f"{a.shape} M={a.m} {a.scheme} cfg={a.cfg} ctas={int(ctas.sum())}  (us relative to first CTA start)")
+for slot in sorted(NAMES):
+    col = d[:, slot]
+    v = col[col > 0]
+    if v.size == 0:
+        continue
+    r = (v - t0) / 1e3
+    print(f"  {NAMES[slot]:>10s}: n={v.size:4d} min={r.min():8.2f} med={np.median(r):8.2f} max={r.max():8.2f}")
