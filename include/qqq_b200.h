@@ -86,42 +86,43 @@ int qqq_dequantize(const int8_t* codes, int64_t K, int64_t N, int64_t group, con
 
 /* ---- one-time repack into the tcgen05 kernel layout ---------------------- */
 
-size_t qqq_repacked_weight_bytes(int mode, int64_t K, int64_t N);
-size_t qqq_repacked_scale_bytes(int64_t K, int64_t N, int64_t group);
+/* Bytes of the kernel-layout weight blob (layout: DESIGN.md / qqq_layout.cuh).
+ * 0 if (mode, group) is not a kernel layout (per-group needs group in {32, 64}
+ * or a multiple of 128; other group sizes use QQQ_MODE_I8). */
+size_t qqq_repacked_weight_bytes(int mode, int64_t K, int64_t N, int64_t group);
 
-/* QQQ_MODE_PC / QQQ_MODE_PG nibble layouts from the reference pack_i4 bytes. */
-int qqq_repack_weights(const uint8_t* packed, int64_t K, int64_t N, int mode, void* out, qqq_stream_t stream);
+/* QQQ_MODE_PC / QQQ_MODE_PG blob from the reference pack_i4 bytes (+ the fused
+ * binary16 s_star [K/group x N] for PG). For PG, flags_dev gets
+ * QQQ_STAT_NEED_CLAMP if, for the codes actually present, the clamp-free HFMA2
+ * converter would differ from the reference's clamped FusedDequantQuant
+ * (gemm.py:123-127); the caller then builds the QQQ_MODE_I8 blob instead. */
+int qqq_repack_weights(const uint8_t* packed, const uint16_t* s_star, int64_t K, int64_t N, int mode, int64_t group,
+                       void* out, int32_t* flags_dev, qqq_stream_t stream);
 
-/* QQQ_MODE_I8 layout from an int8 K x N matrix (w8), or from pack_i4 bytes +
+/* QQQ_MODE_I8 blob from an int8 K x N matrix (w8), or from pack_i4 bytes +
  * s_star via the reference's exact scalar FusedDequantQuant (gemm.py:110-127). */
 int qqq_repack_weights_i8(const int8_t* w8, const uint8_t* packed, const uint16_t* s_star, int64_t group, int64_t K,
                           int64_t N, void* out, qqq_stream_t stream);
 
-/* s_star [K/group x N] -> per-tile layout; sets QQQ_STAT_NEED_CLAMP in
- * flags_dev if, for the codes actually present in some group (packed, the
- * pack_i4 bytes; NULL = assume all 16 codes), the clamp-free HFMA2 converter
- * would differ from the reference's clamped FusedDequantQuant. */
-int qqq_repack_scales(const uint16_t* s_star, const uint8_t* packed, int64_t K, int64_t N, int64_t group, void* out,
-                      int32_t* flags_dev, qqq_stream_t stream);
-
 /* ---- the W4A8 GEMM ------------------------------------------------------- */
 
-/* Caller-provided zero-initialised workspace; the kernels leave it zeroed. */
+/* Caller-provided workspace, zero-initialised once; every launch leaves its
+ * counter head zeroed again (launches sharing it must be stream-ordered). */
 size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K);
 
 /* w4a8_gemm_per_channel (gemm.py:173-185): y f16 M x N = f16((acc*s_a)*s_w_folded),
  * acc = aq . (16*q). acc_opt (int32 M x N) is written when non-NULL. aq must be
- * 16-byte aligned with ldq % 16 == 0. */
+ * 16-byte aligned with ldq % 16 == 0 and ldq >= round_up(K, 128) (bytes past K
+ * in a row are read but multiply zero weights). */
 int qqq_w4a8_gemm_pc(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
                      const double* s_w_folded, int64_t M, int64_t N, int64_t K, void* y, int64_t ldy, int32_t* acc_opt,
                      int64_t ldacc, void* workspace, size_t ws_bytes, qqq_stream_t stream);
 
 /* w4a8_gemm_per_group (gemm.py:188-203): acc = aq . FusedDequantQuant(q, s*),
- * y = f16((acc*s_a)*s_wc). group in {32, 64, 128} or a multiple of 256. */
-int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
-                     const void* s_star_repacked, int64_t group, const double* s_wc, int64_t M, int64_t N, int64_t K,
-                     void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
-                     qqq_stream_t stream);
+ * y = f16((acc*s_a)*s_wc); the blob carries s*. group in {32, 64} or k*128. */
+int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked, int64_t group,
+                     const double* s_wc, int64_t M, int64_t N, int64_t K, void* y, int64_t ldy, int32_t* acc_opt,
+                     int64_t ldacc, void* workspace, size_t ws_bytes, qqq_stream_t stream);
 
 /* Generic form (mode PC/PG/I8) with an optional tile-plan override; I8 with
  * s_col == NULL is gemm_i8_i32 (gemm.py:145-154, acc only). */
@@ -133,9 +134,9 @@ typedef struct qqq_gemm_config {
 } qqq_gemm_config;
 
 int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
-                     const void* sc_repacked, int64_t group, const double* s_col, int64_t M, int64_t N, int64_t K,
-                     void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
-                     const qqq_gemm_config* cfg, qqq_stream_t stream);
+                     int64_t group, const double* s_col, int64_t M, int64_t N, int64_t K, void* y, int64_t ldy,
+                     int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes, const qqq_gemm_config* cfg,
+                     qqq_stream_t stream);
 
 /* ---- conversion test hooks (the exact device functions the GEMM uses) ---- */
 

@@ -37,15 +37,13 @@ SIGNATURES = {
     "qqq_unpack_i4": (c_int, [P, I64, I64, P, P, S]),
     "qqq_fused_scales_pg": (c_int, [P, P, I64, I64, P, P, S]),
     "qqq_dequantize": (c_int, [P, I64, I64, I64, P, P, S]),
-    "qqq_repacked_weight_bytes": (c_size_t, [c_int, I64, I64]),
-    "qqq_repacked_scale_bytes": (c_size_t, [I64, I64, I64]),
-    "qqq_repack_weights": (c_int, [P, I64, I64, c_int, P, S]),
+    "qqq_repacked_weight_bytes": (c_size_t, [c_int, I64, I64, I64]),
+    "qqq_repack_weights": (c_int, [P, P, I64, I64, c_int, I64, P, P, S]),
     "qqq_repack_weights_i8": (c_int, [P, P, P, I64, I64, I64, P, S]),
-    "qqq_repack_scales": (c_int, [P, P, I64, I64, I64, P, P, S]),
     "qqq_gemm_workspace_bytes": (c_size_t, [I64, I64, I64]),
     "qqq_w4a8_gemm_pc": (c_int, [P, I64, P, P, P, I64, I64, I64, P, I64, P, I64, P, c_size_t, S]),
-    "qqq_w4a8_gemm_pg": (c_int, [P, I64, P, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t, S]),
-    "qqq_w4a8_gemm_ex": (c_int, [c_int, P, I64, P, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t,
+    "qqq_w4a8_gemm_pg": (c_int, [P, I64, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t, S]),
+    "qqq_w4a8_gemm_ex": (c_int, [c_int, P, I64, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t,
                                   ctypes.POINTER(GemmConfig), S]),
     "qqq_test_fused_dequant_quant": (c_int, [P, P, P, I64, c_int, S]),
     "qqq_test_pc_convert": (c_int, [P, P, I64, S]),

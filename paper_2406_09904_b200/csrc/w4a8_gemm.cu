@@ -8,19 +8,24 @@
 //
 // Design (weight-stationary, tokens on the MMA N axis):
 //   * UMMA M = 128 output channels per tile, UMMA N = NTOK tokens (16..256),
-//     int8 x int8 -> int32 accumulators in TMEM (tcgen05.mma kind::i8).
-//   * Warp roles (512 threads): w0 = TMA/bulk producer, w1 = MMA issuer,
-//     w2 = TMEM allocator, w4-7 = epilogue (one TMEM lane quadrant each),
-//     w8-15 = INT4->INT8 converters (shift for PC, HFMA2 magic-number
-//     FusedDequantQuant for PG) writing the canonical no-swizzle K-major
-//     operand into shared memory.
-//   * Activations: 2-D TMA (SWIZZLE_128B, OOB rows zero-filled) of the int8
-//     [M, K] codes; weights: 1-D cp.async.bulk of contiguous repacked k-blocks.
-//   * Work split: stream-K over (tile, k-block) units across the 148 SMs; split
-//     tiles reduce their int32 partials with red.global.add (integer, so the
-//     result is order-free and bit-exact) and the last arriving CTA applies the
-//     epilogue and re-zeroes the workspace. Unsplit tiles go straight to the
-//     epilogue from TMEM (double-buffered accumulators).
+//     int8 x int8 -> int32 accumulators in TMEM (tcgen05.mma kind::i8),
+//     double-buffered so the epilogue of one tile overlaps the next tile's MMAs.
+//   * Warp roles (512 threads). The SM sub-partition scheduler issues from the
+//     highest warp id first, so latency-critical single-thread roles get the
+//     high ids: w15 = MMA issuer, w14 = TMA/bulk producer, w12 = TMEM allocator,
+//     w8-11 = epilogue (TMEM lane quadrant = warp % 4), w0-7 = INT4->INT8
+//     converters (shift for PC, HFMA2 magic-number FusedDequantQuant for PG)
+//     writing the canonical no-swizzle K-major operand into shared memory.
+//   * Per k-block exactly two TMA ops: one cp.async.bulk of the contiguous
+//     weight(+scale) super-slabs and one 3-D tensor TMA of the int8 activation
+//     tile (SWIZZLE_128B, OOB token rows zero-filled).
+//   * PDL: the first kStages k-blocks of weights are requested before
+//     griddepcontrol.wait, overlapping the previous kernel's tail.
+//   * Work split: stream-K over (tile, k-block) units across the SMs. A tile
+//     split over several CTAs is reduced exactly: each segment stores its int32
+//     partial to its own workspace slot, the last arriving CTA (atomic counter)
+//     sums the slots (integer addition: order-free, bit-exact) and applies the
+//     epilogue; counters are re-zeroed by that CTA.
 //   * Epilogue: f64 (acc * s_a) * s_col then cvt.rn.f16.f64 -> bit-identical
 //     to the reference's f64 epilogue with a single final rounding.
 #include <cstdio>
@@ -32,55 +37,47 @@
 namespace qqq {
 
 constexpr int kNumThreads = 512;
-constexpr int kEpiWarp0 = 4, kNumEpiWarps = 4;
-constexpr int kConvWarp0 = 8, kNumConvWarps = 8;
+constexpr int kConvWarp0 = 0, kNumConvWarps = 8;
+constexpr int kEpiWarp0 = 8, kNumEpiWarps = 4;
+constexpr int kAllocWarp = 12;
+constexpr int kProducerWarp = 14;
+constexpr int kMmaWarp = 15;
 constexpr int kSmemBudget = 225 * 1024;
+constexpr int kDbgSlots = 64;
 
 struct GemmParams {
-  const uint8_t* w;    // repacked weights (layout in qqq_layout.cuh)
-  const __half* sc;    // PG: repacked s* [n_tiles][G_pad][128]
-  const double* s_a;   // [M]
-  const double* s_col; // [N] s_w_folded (PC) / s_wc (PG); nullptr -> acc only
+  const uint8_t* w;     // repacked weight blob (qqq_layout.cuh)
+  const double* s_a;    // [M]
+  const double* s_col;  // [N] s_w_folded (PC) / s_wc (PG); nullptr -> acc only
   __half* y;
   int64_t ldy;
   int32_t* acc;  // optional
   int64_t ldacc;
-  int32_t* ws;        // [tiles][NTOK][128] int32, zero on entry and exit
-  int32_t* counters;  // [tiles], zero on entry and exit
+  int32_t* ws;        // split-K partials [tiles][max_segs][NTOK][128] int32 (no init needed)
+  int32_t* counters;  // [tiles] arrival counters at the fixed head of the workspace; zero on entry and exit
   int M, N, K;
-  int n_tiles, tok_tiles, kb_per_tile, slabs, g_pad, group;
+  int n_tiles, tok_tiles, kb_per_tile, ss_per_tile, ss_bytes, group, max_segs;
   int64_t units;
-  int aligned_tiles;  // >0: CTA b owns whole tiles [b*aligned_tiles, ...)
-  unsigned long long* dbg;  // optional per-CTA timeline (kDbgSlots %globaltimer stamps), diagnostics only
+  int aligned_tiles;        // >0: CTA b owns whole tiles [b*aligned_tiles, ...)
+  unsigned long long* dbg;  // optional per-CTA %globaltimer timeline, diagnostics only
 };
-
-constexpr int kDbgSlots = 64;
-QQQ_DEVICE unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define QQQ_STAMP(slot)                                                          \
-  do {                                                                           \
-    if (p.dbg) p.dbg[(size_t)blockIdx.x * kDbgSlots + (slot)] = gtimer();        \
-  } while (0)
 
 template <int MODE, int NTOK, int BK>
 struct Cfg {
   static constexpr bool kConvert = MODE != kModeI8;
   static constexpr int kActBytes = NTOK * BK;
-  static constexpr int kWBytes = (MODE == kModeI8) ? BK * 128 : BK * 64;
-  static constexpr int kScBytes = (MODE == kModePG) ? (BK / 32) * 256 : 0;
+  // worst-case super-slab bytes (PG with g = 32) for the smem carve-up
+  static constexpr int kSSMax = MODE == kModeI8 ? 16384 : MODE == kModePC ? 8192 : 8192 + 256 * 4;
+  static constexpr int kWBytes = (BK / 128) * kSSMax;
   static constexpr int kABytes = BK * 128;
   static constexpr int kABufs = kConvert ? 2 : 0;
-  static constexpr int kStageBytes = kActBytes + kWBytes + kScBytes;
+  static constexpr int kStageBytes = kActBytes + kWBytes;
   static constexpr int kStagesRaw = (kSmemBudget - 4096 - kABufs * kABytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static_assert(kStages >= 2, "shared memory budget too small");
-  static constexpr int kOffAct = 0;
+  static constexpr int kOffAct = 0;  // 1024-aligned: NTOK*BK is a multiple of 2048
   static constexpr int kOffW = kOffAct + kStages * kActBytes;
-  static constexpr int kOffSc = kOffW + kStages * kWBytes;
-  static constexpr int kOffA = (kOffSc + kStages * kScBytes + 1023) / 1024 * 1024;
+  static constexpr int kOffA = (kOffW + kStages * kWBytes + 1023) / 1024 * 1024;
   static constexpr int kOffBar = kOffA + kABufs * kABytes;
   static constexpr int kNumBars = 2 * kStages + 2 * kABufs + 4;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // +1024 alignment slack
@@ -91,8 +88,20 @@ struct Cfg {
   static_assert(BK % 128 == 0, "BK must be a multiple of the 128-byte swizzle atom");
 };
 
-// Programmatic dependent launch (PDL): wait for / release the neighbouring
-// kernels in the stream. No-ops when launched without the PDL attribute.
+// ---------------------------------------------------------------------------
+// small device helpers
+// ---------------------------------------------------------------------------
+QQQ_DEVICE unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define QQQ_STAMP(slot)                                                   \
+  do {                                                                    \
+    if (p.dbg) p.dbg[(size_t)blockIdx.x * kDbgSlots + (slot)] = gtimer(); \
+  } while (0)
+
+// Programmatic dependent launch (PDL). No-ops without the launch attribute.
 QQQ_DEVICE void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 QQQ_DEVICE void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -104,19 +113,24 @@ QQQ_DEVICE __half f64_to_f16_rn(double v) {
   return __ushort_as_half(h);
 }
 
-QQQ_DEVICE void red_add_s32(int32_t* p, int32_t v) {
-  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+QQQ_DEVICE void tma_load_3d(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
+                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
 }
 
-// Dequant epilogue for 16 consecutive tokens of one output channel n:
+// Dequant epilogue for up to 16 consecutive tokens of one output channel n:
 // y = f16((acc * s_a[t]) * s_col[n]) in f64 with one final RN rounding
 // (gemm.py:182-184 / 200-202); acc written as-is when requested.
 QQQ_DEVICE void store_outputs(const GemmParams& p, const uint32_t (&r)[16], int t0, int nvalid, int n, bool n_ok,
                               double s_col) {
+  if (!n_ok) return;
   double sa[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) sa[i] = (i < nvalid) ? __ldg(p.s_a + t0 + i) : 0.0;
-  if (!n_ok) return;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     if (i < nvalid) {
@@ -128,7 +142,7 @@ QQQ_DEVICE void store_outputs(const GemmParams& p, const uint32_t (&r)[16], int 
   }
 }
 
-// Segment iterator: the contiguous unit range of this CTA split at tile borders.
+// Segment iterator: the CTA's contiguous (tile, k-block) unit range split at tile borders.
 struct SegIter {
   int64_t u, u1;
   int kbt;
@@ -136,7 +150,7 @@ struct SegIter {
     if (u >= u1) return false;
     tile = (int)(u / kbt);
     kb0 = (int)(u % kbt);
-    int64_t rem = u1 - u;
+    const int64_t rem = u1 - u;
     kb1 = (int)((kbt - kb0) < rem ? kbt : kb0 + rem);
     u += kb1 - kb0;
     return true;
@@ -147,11 +161,13 @@ QQQ_DEVICE SegIter make_iter(const GemmParams& p) {
   SegIter it;
   it.kbt = p.kb_per_tile;
   if (p.aligned_tiles > 0) {
+    const int64_t tiles = (int64_t)p.n_tiles * p.tok_tiles;
     int64_t t0 = (int64_t)blockIdx.x * p.aligned_tiles;
-    int64_t tiles = (int64_t)p.n_tiles * p.tok_tiles;
     int64_t t1 = t0 + p.aligned_tiles < tiles ? t0 + p.aligned_tiles : tiles;
+    if (t0 > tiles) t0 = tiles;
+    if (t1 < t0) t1 = t0;
     it.u = t0 * p.kb_per_tile;
-    it.u1 = (t1 > t0 ? t1 : t0) * p.kb_per_tile;
+    it.u1 = t1 * p.kb_per_tile;
   } else {
     it.u = (int64_t)blockIdx.x * p.units / gridDim.x;
     it.u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
@@ -159,6 +175,14 @@ QQQ_DEVICE SegIter make_iter(const GemmParams& p) {
   return it;
 }
 
+// stream-K: the CTA whose unit range contains unit u (start(b) = floor(b*U/G))
+QQQ_DEVICE int cta_of_unit(int64_t u, int64_t units, int grid) {
+  return (int)(((u + 1) * grid - 1) / units);
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
 template <int MODE, int NTOK, int BK>
 __global__ void __launch_bounds__(kNumThreads, 1)
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const GemmParams p) {
@@ -178,8 +202,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  if (threadIdx.x == 0) QQQ_STAMP(0);
   if (threadIdx.x == 0) {
+    QQQ_STAMP(0);
+    griddep_launch_dependents();
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::kConvert ? kNumConvWarps + 1 : 1);
@@ -194,50 +219,32 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     mbar_fence_init();
   }
-  if (warp == 0 && lane == 0) tma_prefetch_desc(&act_map);
-  if (threadIdx.x == 0) griddep_launch_dependents();
-  if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == kProducerWarp && lane == 0) tma_prefetch_desc(&act_map);
+  if (warp == kAllocWarp) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) QQQ_STAMP(1);
+  const int wbytes = (BK / 128) * p.ss_bytes;  // this launch's weight bytes per k-block
+  const uint32_t stage_tx = (uint32_t)(C::kActBytes + wbytes);
 
-  if (warp == 0) {
+  if (warp == kProducerWarp) {
     // ======================= TMA / bulk producer =======================
-    // Weights and scales do not depend on the previous kernel in the stream, so
-    // the first kStages k-blocks of weights are requested BEFORE the PDL grid
-    // dependency wait; only the activation loads wait for the producer kernel.
     if (lane == 0) {
+      QQQ_STAMP(1);
       auto issue_weights = [&](int n_tile, int kb, int s) {
-        const int64_t slab0 = (int64_t)n_tile * p.slabs + (int64_t)kb * (BK / 32);
-        const int64_t wofs = slab0 * (MODE == kModeI8 ? 4096 : 2048);
-        bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + wofs, C::kWBytes, &full[s]);
-        if constexpr (MODE == kModePG) {
-          // groups covered by this k-block (g <= BK: BK/g groups; g > BK: one)
-          const int g = p.group;
-          const int gfirst = (int)(((int64_t)kb * BK) / g);
-          const int bytes = (g <= BK ? BK / g : 1) * 256;
-          const __half* src = p.sc + ((int64_t)n_tile * p.g_pad + gfirst) * 128;
-          // the stage always receives kScBytes so expect_tx is constant: repeat the copy
-          for (int off = 0; off < C::kScBytes; off += bytes)
-            bulk_g2s(smem + C::kOffSc + s * C::kScBytes + off, src, bytes, &full[s]);
-        }
-      };
-      auto issue_act = [&](int tok0, int kb, int s) {
-        uint8_t* act = smem + C::kOffAct + s * C::kActBytes;
-#pragma unroll
-        for (int j = 0; j < BK / 128; ++j)
-          tma_load_2d(act + j * NTOK * 128, &act_map, kb * BK + j * 128, tok0, &full[s]);
+        const int64_t ss0 = (int64_t)n_tile * p.ss_per_tile + (int64_t)kb * (BK / 128);
+        bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &full[s]);
       };
       int tile, kb0, kb1;
-      // pass 1: arm the first kStages stages and stream their weights
+      // pass 1: weights do not depend on the previous kernel -> stream them
+      // into the first kStages stages before the PDL grid-dependency wait
       uint32_t pre = 0;
       {
         SegIter si = make_iter(p);
         while (pre < (uint32_t)C::kStages && si.next(tile, kb0, kb1)) {
           for (int kb = kb0; kb < kb1 && pre < (uint32_t)C::kStages; ++kb, ++pre) {
-            mbar_arrive_expect_tx(&full[pre], C::kStageBytes);
+            mbar_arrive_expect_tx(&full[pre], stage_tx);
             issue_weights(tile / p.tok_tiles, kb, pre);
           }
         }
@@ -255,14 +262,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           const int s = it % C::kStages;
           if (it >= pre) {
             mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
-            mbar_arrive_expect_tx(&full[s], C::kStageBytes);
+            mbar_arrive_expect_tx(&full[s], stage_tx);
             issue_weights(n_tile, kb, s);
           }
-          issue_act(tok0, kb, s);
+          tma_load_3d(smem + C::kOffAct + s * C::kActBytes, &act_map, 0, tok0, kb * (BK / 128), &full[s]);
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ============================ MMA issuer ============================
     if (lane == 0) {
       SegIter si = make_iter(p);
@@ -291,7 +298,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           for (int kk = 0; kk < BK / 32; ++kk) {
             // A: canonical K-major, no swizzle: [k16 chunk][128 rows][16 B]
             const uint64_t a_desc = make_smem_desc(a_addr + kk * 2 * 2048, 2048, 128, 0);
-            // B: TMA SWIZZLE_128B box [NTOK rows][128 B]; 32 B K-steps inside the atom
+            // B: SWIZZLE_128B [k-atom][NTOK rows][128 B]; 32 B K-steps inside the atom
             const uint32_t b_addr = act_addr + (kk / 4) * (NTOK * 128) + (kk % 4) * 32;
             const uint64_t b_desc = make_smem_desc(b_addr, 16, 1024, 2);
             mma_i8_ss(d_tmem, a_desc, b_desc, C::kIdesc, (kb > kb0 || kk > 0) ? 1u : 0u);
@@ -307,27 +314,30 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         ++seg;
       }
     }
-  } else if (warp >= kConvWarp0) {
+  } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kNumConvWarps) {
     // ====================== INT4 -> INT8 converters ======================
     if constexpr (C::kConvert) {
       const int cw = warp - kConvWarp0;
+      const int geff = p.group < 128 ? p.group : 128;
       SegIter si = make_iter(p);
       int tile, kb0, kb1;
-      uint32_t it = 0, ait = 0;
+      uint32_t it = 0;
       while (si.next(tile, kb0, kb1)) {
-        for (int kb = kb0; kb < kb1; ++kb, ++it, ++ait) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::kStages;
           mbar_wait(&full[s], (it / C::kStages) & 1);
           if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(4 + it);
-          const int b = ait % C::kABufs;
-          mbar_wait(&a_empty[b], ((ait / C::kABufs) & 1) ^ 1);
+          const int b = it % C::kABufs;
+          mbar_wait(&a_empty[b], ((it / C::kABufs) & 1) ^ 1);
           const uint8_t* wst = smem + C::kOffW + s * C::kWBytes;
           uint8_t* abuf = smem + C::kOffA + b * C::kABytes;
 #pragma unroll
-          for (int wu = cw; wu < BK / 8; wu += kNumConvWarps) {
+          for (int i = 0; i < BK / 64; ++i) {
+            const int wu = cw + i * kNumConvWarps;  // warp-unit: 32 rows x one 32-k slab
             const int c = wu >> 2;                  // slab within the k-block
             const int row = ((wu & 3) << 5) + lane;  // channel within the tile
-            const uint4 v = *reinterpret_cast<const uint4*>(wst + (c * 128 + row) * 16);
+            const uint8_t* ssp = wst + (c >> 2) * p.ss_bytes;
+            const uint4 v = *reinterpret_cast<const uint4*>(ssp + ((c & 3) * 128 + row) * 16);
             uint4 o0, o1;
             if constexpr (MODE == kModePC) {
               pc_convert_word(v.x, o0.x, o1.x);
@@ -335,11 +345,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               pc_convert_word(v.z, o0.z, o1.z);
               pc_convert_word(v.w, o0.w, o1.w);
             } else {
-              const int g = p.group;
-              const int lg = g <= BK ? (c * 32) / g : 0;
-              const __half s1 = reinterpret_cast<const __half*>(smem + C::kOffSc + s * C::kScBytes)[lg * 128 + row];
+              const int lg = ((c & 3) * 32) / geff;
+              const __half s1 = reinterpret_cast<const __half*>(ssp + 8192)[lg * 128 + row];
               const __half2 s2 = __halves2half2(s1, s1);
-              const __half2 s16 = __hmul2(s2, u32_as_h2(0x2C002C00u));  // * 1/16, exact for s* >= 2^-10
+              const __half2 s16 = __hmul2(s2, u32_as_h2(0x2C002C00u));  // * 1/16
               pg_convert_word<false>(v.x, s2, s16, o0.x, o0.y);
               pg_convert_word<false>(v.y, s2, s16, o0.z, o0.w);
               pg_convert_word<false>(v.z, s2, s16, o1.x, o1.y);
@@ -359,9 +368,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpiWarps) {
     // ============================== epilogue ==============================
-    griddep_wait();  // y / acc / workspace / s_a may be touched by the previous kernel
+    griddep_wait();  // y / acc / workspace / counters / s_a may belong to the previous kernel
     const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = q * 32 + lane;
+    const bool lead = (warp == kEpiWarp0 && lane == 0);
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
     uint32_t seg = 0;
@@ -369,7 +379,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int j = seg & 1;
       mbar_wait(&acc_full[j], (seg >> 1) & 1);
       tc_fence_after();
-      if (threadIdx.x == kEpiWarp0 * 32 && seg < 4) QQQ_STAMP(36 + 2 * seg);
+      if (lead && seg < 4) QQQ_STAMP(36 + 2 * seg);
       const int n_tile = tile / p.tok_tiles;
       const int tok0 = (tile % p.tok_tiles) * NTOK;
       const int n = n_tile * 128 + row;
@@ -377,9 +387,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int tvalid = (p.M - tok0) < NTOK ? (p.M - tok0) : NTOK;
       const bool whole = (kb0 == 0 && kb1 == p.kb_per_tile);
       const double s_col = (n_ok && p.s_col) ? p.s_col[n] : 0.0;
-      int32_t* ws_tile = p.ws + (int64_t)tile * NTOK * 128;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
-      const int nchunks = (tvalid + 15) / 16;  // TMEM columns past the last token are never read
+      const int nchunks = (tvalid + 15) / 16;  // every tile has >= 1 valid token
+      int seg_idx = 0, nsegs = 1;
+      int32_t* slot = nullptr;
+      if (!whole) {
+        const int64_t u_first = (int64_t)tile * p.kb_per_tile;
+        const int b_first = cta_of_unit(u_first, p.units, gridDim.x);
+        const int b_last = cta_of_unit(u_first + p.kb_per_tile - 1, p.units, gridDim.x);
+        seg_idx = (int)blockIdx.x - b_first;
+        nsegs = b_last - b_first + 1;
+        slot = p.ws + ((int64_t)tile * p.max_segs + seg_idx) * NTOK * 128;
+      }
 #pragma unroll 1
       for (int c = 0; c < nchunks; ++c) {
         const int c0 = c * 16;
@@ -396,48 +415,46 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         } else {
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            if (c0 + i < tvalid) red_add_s32(ws_tile + (c0 + i) * 128 + row, (int32_t)r[i]);
+            if (c0 + i < tvalid) __stcg(slot + (c0 + i) * 128 + row, (int32_t)r[i]);
         }
-      }
-      if (nchunks == 0) {  // (cannot happen: every tile has >= 1 token) keep the barrier protocol intact
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[j]);
       }
       if (!whole) {
         __threadfence();
         named_bar_sync(1, kNumEpiWarps * 32);
-        if (warp == kEpiWarp0 && lane == 0) {
-          const int add = kb1 - kb0;
-          const int old = atomicAdd(p.counters + tile, add);
-          *last_flag = (old + add == p.kb_per_tile) ? 1 : 0;
+        if (lead) {
+          const int old = atomicAdd(p.counters + tile, 1);
+          *last_flag = (old + 1 == nsegs) ? 1 : 0;
         }
         named_bar_sync(1, kNumEpiWarps * 32);
         const bool last = *last_flag != 0;
-        named_bar_sync(1, kNumEpiWarps * 32);  // everyone has read last_flag before it is reused
+        named_bar_sync(1, kNumEpiWarps * 32);  // last_flag is reused by the next segment
         if (last) {
           __threadfence();
+          if (lead) p.counters[tile] = 0;
+          const int32_t* base = p.ws + (int64_t)tile * p.max_segs * NTOK * 128;
 #pragma unroll 1
           for (int c0 = 0; c0 < tvalid; c0 += 16) {
             uint32_t r[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              r[i] = (c0 + i < tvalid) ? (uint32_t)__ldcg(ws_tile + (c0 + i) * 128 + row) : 0u;
+            for (int i = 0; i < 16; ++i) r[i] = 0u;
+#pragma unroll 1
+            for (int sg = 0; sg < nsegs; ++sg) {
+              const int32_t* src = base + (int64_t)sg * NTOK * 128 + row;
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (c0 + i < tvalid) __stcg(ws_tile + (c0 + i) * 128 + row, 0);
+              for (int i = 0; i < 16; ++i)
+                if (c0 + i < tvalid) r[i] += (uint32_t)__ldcg(src + (c0 + i) * 128);
+            }
             store_outputs(p, r, tok0 + c0, tvalid - c0, n, n_ok, s_col);
           }
-          if (warp == kEpiWarp0 && lane == 0) p.counters[tile] = 0;
         }
       }
-      if (threadIdx.x == kEpiWarp0 * 32 && seg < 4) QQQ_STAMP(37 + 2 * seg);
+      if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
       ++seg;
     }
   }
 
   __syncthreads();
-  if (threadIdx.x == 0) QQQ_STAMP(63);
-  if (warp == 2) {
+  if (warp == kAllocWarp) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);
   }
@@ -475,7 +492,7 @@ static int num_sms() {
 }
 
 struct LaunchPlan {
-  int ntok, bk, grid, aligned_tiles, tok_tiles, n_tiles, kb_per_tile, tiles;
+  int ntok, bk, grid, aligned_tiles, tok_tiles, n_tiles, kb_per_tile, tiles, max_segs;
   int64_t units;
 };
 
@@ -497,18 +514,32 @@ static LaunchPlan make_plan(int64_t M, int64_t N, int64_t K, int force_ntok, int
   lp.tiles = lp.n_tiles * lp.tok_tiles;
   lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
   const int sms = num_sms();
-  // stream-K for small token tiles (cheap int32 fix-up), whole tiles otherwise
   bool streamk = force_split >= 0 ? force_split == 1 : (lp.ntok <= 64 || lp.tiles < sms / 2);
+  lp.max_segs = 1;
   if (streamk) {
     lp.aligned_tiles = 0;
     lp.grid = (int)(lp.units < sms ? lp.units : sms);
     if (force_grid > 0) lp.grid = (int)(force_grid < lp.units ? force_grid : lp.units);
+    // most CTAs overlapping one tile
+    const int64_t per = lp.units / lp.grid;  // >= 1
+    lp.max_segs = (int)((lp.kb_per_tile + per - 1) / per + 1);
+    if (lp.max_segs > lp.grid) lp.max_segs = lp.grid;
   } else {
-    int per = (lp.tiles + sms - 1) / sms;
+    const int per = (lp.tiles + sms - 1) / sms;
     lp.aligned_tiles = per;
     lp.grid = (lp.tiles + per - 1) / per;
   }
   return lp;
+}
+
+// Workspace = [kMaxTiles int32 counters (fixed head, zero between launches)]
+//             [split-K partial slots of the current plan (never need zeroing)].
+constexpr int kMaxTiles = 65536;
+constexpr size_t kCounterBytes = (size_t)kMaxTiles * 4;
+
+static size_t plan_ws_bytes(const LaunchPlan& lp) {
+  if (lp.aligned_tiles > 0) return kCounterBytes;
+  return kCounterBytes + (size_t)lp.tiles * lp.max_segs * lp.ntok * 128 * 4;
 }
 
 template <int MODE, int NTOK, int BK>
@@ -552,11 +583,10 @@ using namespace qqq;
 
 extern "C" size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
-  // worst case over configs: every tile of the smallest-padding plan
-  size_t best = 0;
+  size_t best = 0;  // any plan a caller may force
   for (int nt : {16, 32, 64, 128, 256}) {
-    int64_t tt = (M + nt - 1) / nt;
-    size_t b = (size_t)round_up(N, kTileN) * tt * nt * 4 + (size_t)(round_up(N, kTileN) / kTileN) * tt * 4 + 256;
+    LaunchPlan lp = make_plan(M, N, K, nt, 0, 1);
+    size_t b = plan_ws_bytes(lp);
     if (b > best) best = b;
   }
   return best;
@@ -564,55 +594,56 @@ extern "C" size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
 
 // Generic entry: mode 0 = per-channel (PC), 1 = per-group (PG), 2 = pre-converted int8 (I8).
 extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
-                                const void* sc_repacked, int64_t group, const double* s_col, int64_t M, int64_t N,
-                                int64_t K, void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace,
-                                size_t ws_bytes, const qqq_gemm_config* cfg, cudaStream_t stream) {
+                                int64_t group, const double* s_col, int64_t M, int64_t N, int64_t K, void* y,
+                                int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
+                                const qqq_gemm_config* cfg, cudaStream_t stream) {
   if (M < 0 || N <= 0 || K <= 0) return kErrShape;
   if (K > (1 << 16)) return kErrShape;  // gemm.py:49,151
   if (M == 0) return kOk;
-  if (mode == kModePG && (group <= 0 || !(group % 256 == 0 || (group <= 128 && 128 % group == 0 && group % 32 == 0))))
+  if (mode == kModePG && !pg_group_ok(group)) return kErrUnsupported;
+  // 3-D activation view {128, M, ceil(K/128)}: rows must hold round_up(K, 128) bytes
+  if ((ldq % 16) != 0 || ldq < round_up(K, 128) || (reinterpret_cast<uintptr_t>(aq) & 15) != 0)
     return kErrUnsupported;
-  if (mode == kModePG && !sc_repacked) return kErrConfig;
-  if ((ldq % 16) != 0 || (reinterpret_cast<uintptr_t>(aq) & 15) != 0) return kErrUnsupported;
   if (s_col && (!y || ldy < N)) return kErrShape;
   if (!s_col && !acc_opt) return kErrConfig;
-  if (ws_bytes < qqq_gemm_workspace_bytes(M, N, K)) return kErrConfig;
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return kErrCuda;
 
   LaunchPlan lp = make_plan(M, N, K, cfg ? cfg->ntok : 0, cfg ? cfg->grid : 0, cfg ? cfg->split : -1);
+  if (lp.tiles > kMaxTiles) return kErrUnsupported;
+  if (ws_bytes < plan_ws_bytes(lp)) return kErrConfig;
 
   CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
-  cuuint64_t strides[1] = {(cuuint64_t)ldq};
-  cuuint32_t box[2] = {128u, (cuuint32_t)lp.ntok};
-  cuuint32_t estr[2] = {1u, 1u};
-  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)aq, dims, strides, box, estr,
+  const int64_t katoms = (K + 127) / 128;
+  cuuint64_t dims[3] = {128u, (cuuint64_t)M, (cuuint64_t)katoms};
+  cuuint64_t strides[2] = {(cuuint64_t)ldq, 128u};
+  cuuint32_t box[3] = {128u, (cuuint32_t)lp.ntok, (cuuint32_t)(lp.bk / 128)};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)aq, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return kErrCuda;
 
   GemmParams p{};
   p.w = (const uint8_t*)w_repacked;
-  p.sc = (const __half*)sc_repacked;
   p.s_a = s_a;
   p.s_col = s_col;
   p.y = (__half*)y;
   p.ldy = ldy;
   p.acc = acc_opt;
   p.ldacc = ldacc;
-  const size_t ws_main = (size_t)lp.tiles * lp.ntok * 128 * 4;
-  p.ws = (int32_t*)workspace;
-  p.counters = (int32_t*)((uint8_t*)workspace + ws_main);
+  p.counters = (int32_t*)workspace;
+  p.ws = (int32_t*)((uint8_t*)workspace + kCounterBytes);
   p.M = (int)M;
   p.N = (int)N;
   p.K = (int)K;
   p.n_tiles = lp.n_tiles;
   p.tok_tiles = lp.tok_tiles;
   p.kb_per_tile = lp.kb_per_tile;
-  p.slabs = (int)(round_up(K, kKPadTo) / kSlabK);
+  p.ss_per_tile = (int)(round_up(K, kKPadTo) / kSuperK);
+  p.ss_bytes = (int)ss_bytes(mode, group);
   p.group = (int)group;
-  p.g_pad = group > 0 ? (int)((round_up(K, kKPadTo) + group - 1) / group) : 0;
+  p.max_segs = lp.max_segs;
   p.units = lp.units;
   p.aligned_tiles = lp.aligned_tiles;
   p.dbg = cfg ? (unsigned long long*)cfg->dbg : nullptr;
@@ -628,14 +659,14 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
 extern "C" int qqq_w4a8_gemm_pc(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
                                 const double* s_w_folded, int64_t M, int64_t N, int64_t K, void* y, int64_t ldy,
                                 int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes, cudaStream_t stream) {
-  return qqq_w4a8_gemm_ex(kModePC, aq, ldq, s_a, w_repacked, nullptr, 0, s_w_folded, M, N, K, y, ldy, acc_opt, ldacc,
+  return qqq_w4a8_gemm_ex(kModePC, aq, ldq, s_a, w_repacked, 0, s_w_folded, M, N, K, y, ldy, acc_opt, ldacc,
                           workspace, ws_bytes, nullptr, stream);
 }
 
 extern "C" int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
-                                const void* s_star_repacked, int64_t group, const double* s_wc, int64_t M, int64_t N,
-                                int64_t K, void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace,
-                                size_t ws_bytes, cudaStream_t stream) {
-  return qqq_w4a8_gemm_ex(kModePG, aq, ldq, s_a, w_repacked, s_star_repacked, group, s_wc, M, N, K, y, ldy, acc_opt,
-                          ldacc, workspace, ws_bytes, nullptr, stream);
+                                int64_t group, const double* s_wc, int64_t M, int64_t N, int64_t K, void* y,
+                                int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
+                                cudaStream_t stream) {
+  return qqq_w4a8_gemm_ex(kModePG, aq, ldq, s_a, w_repacked, group, s_wc, M, N, K, y, ldy, acc_opt, ldacc,
+                          workspace, ws_bytes, nullptr, stream);
 }

@@ -115,9 +115,9 @@ QQQ_DEVICE int ref_nibble(const uint8_t* packed, int64_t K, int64_t N, int64_t k
   return (k & 1) ? (b >> 4) : (b & 0xF);
 }
 
-// One thread per (n_pad, slab): 32 nibbles of one channel -> 16 B of the PC/PG layout.
+// One thread per (n_pad, slab): 32 nibbles of one channel -> 16 B of the PC/PG blob.
 __global__ void repack4_kernel(const uint8_t* __restrict__ packed, int64_t K, int64_t N, int64_t N_pad, int64_t slabs,
-                               int mode, uint8_t* __restrict__ out) {
+                               int mode, int64_t ssb, uint8_t* __restrict__ out) {
   const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t slab = blockIdx.y;
   if (n >= N_pad) return;
@@ -138,13 +138,52 @@ __global__ void repack4_kernel(const uint8_t* __restrict__ packed, int64_t K, in
     wd[i] = v;
   }
   const int64_t n_tile = n / kTileN, row = n % kTileN;
-  uint4* dst = reinterpret_cast<uint4*>(out + ((n_tile * slabs + slab) * kTileN + row) * 16);
+  const int64_t ss = (n_tile * (slabs / 4) + slab / 4);
+  uint4* dst = reinterpret_cast<uint4*>(out + ss * ssb + ((slab % 4) * kTileN + row) * 16);
   *dst = make_uint4(wd[0], wd[1], wd[2], wd[3]);
 }
 
-// One thread per (n_pad, slab, chunk): 16 int8 of the I8 layout. src is either
-// a K x N int8 matrix (mode I8 from int8) or the reference packed bytes + s*
-// (per-group, exact scalar FusedDequantQuant with the reference's clamp).
+// One thread per (n_pad, super-slab, local group): the s* of that group chunk
+// into the PG blob, plus the fast-path admissibility test. The HFMA2 converter
+// omits the reference's clamp (gemm.py:123-127); that is exact iff every code q
+// present gives RN(q*s* + 1152) in [1025, 1279], and by monotonicity in q it
+// suffices to test the chunk's min and max code. Weights from requant_scale
+// always pass (test_gemm.py:273-280). A tiny s* is harmless: |q*s*| < 1/2, so
+// both RN(q*s* + 1152) and the s*/16 form give exactly 1152.
+__global__ void repack_scales_kernel(const uint16_t* __restrict__ s_star, const uint8_t* __restrict__ packed,
+                                     int64_t K, int64_t N, int64_t N_pad, int64_t group, int64_t ssb,
+                                     int64_t ss_per_tile, uint8_t* __restrict__ out, int32_t* flags) {
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int ngs = pg_groups_per_ss(group);
+  const int64_t ss = blockIdx.y / ngs;
+  const int gl = blockIdx.y % ngs;
+  if (n >= N_pad) return;
+  const int64_t geff = group < 128 ? group : 128;
+  const int64_t k0 = ss * 128 + gl * geff;  // first k of this chunk
+  uint16_t h = 0;
+  if (k0 < K && n < N) {
+    h = s_star[(k0 / group) * N + n];
+    int qmin = 7, qmax = -8;
+    for (int64_t k = k0; k < k0 + geff && k < K; ++k) {
+      const int q = ref_nibble(packed, K, N, k, n) - 8;
+      qmin = min(qmin, q);
+      qmax = max(qmax, q);
+    }
+    const __half s = __ushort_as_half(h);
+    const __half add = __float2half_rn(1152.0f);
+    const float r_a = __half2float(__hfma(__int2half_rn(qmin), s, add));
+    const float r_b = __half2float(__hfma(__int2half_rn(qmax), s, add));
+    const float lo = fminf(r_a, r_b), hi = fmaxf(r_a, r_b);
+    if (!(lo >= 1025.0f && hi <= 1279.0f)) atomicOr(flags, kStatNeedClamp);  // NaN fails too
+  }
+  const int64_t n_tile = n / kTileN, row = n % kTileN;
+  uint16_t* dst = reinterpret_cast<uint16_t*>(out + (n_tile * ss_per_tile + ss) * ssb + 8192);
+  dst[gl * kTileN + row] = h;
+}
+
+// One thread per (n_pad, slab, chunk): 16 int8 of the I8 blob. src is either
+// a K x N int8 matrix (w8) or the reference packed bytes + s* (per-group,
+// exact scalar FusedDequantQuant including the reference's clamp).
 __global__ void repack8_kernel(const int8_t* __restrict__ w8, const uint8_t* __restrict__ packed,
                                const uint16_t* __restrict__ s_star, int64_t group, int64_t K, int64_t N, int64_t N_pad,
                                int64_t slabs, uint8_t* __restrict__ out) {
@@ -167,45 +206,9 @@ __global__ void repack8_kernel(const int8_t* __restrict__ w8, const uint8_t* __r
     v[e] = r;
   }
   const int64_t n_tile = n / kTileN, row = n % kTileN;
+  // I8 blob: per tile, consecutive slabs of [2 chunks][128 rows][16 B] (== [k16 chunk][row][16 B])
   *reinterpret_cast<uint4*>(out + (((n_tile * slabs + slab) * 2 + chunk) * kTileN + row) * 16) =
       *reinterpret_cast<const uint4*>(v);
-}
-
-// s*[G][N] -> [n_tiles][G_pad][128] (zero padded) + fast-path admissibility.
-// The HFMA2 converter omits the reference's clamp (gemm.py:123-127), which is
-// exact iff every code q present in group (g, n) gives RN(q*s* + 1152) in
-// [1025, 1279]; by monotonicity in q it suffices to test the group's min and
-// max code. Weights from requant_scale always pass (test_gemm.py:273-280).
-// A tiny s* is harmless: |q*s*| < 1/2 so both RN(q*s*+1152) and the s*/16
-// form give 1152 exactly.
-__global__ void repack_scales_kernel(const uint16_t* __restrict__ s_star, const uint8_t* __restrict__ packed,
-                                     int64_t K, int64_t group, int64_t G, int64_t N, int64_t N_pad, int64_t G_pad,
-                                     uint16_t* __restrict__ out, int32_t* flags) {
-  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t g = blockIdx.y;
-  if (n >= N_pad) return;
-  uint16_t h = 0;
-  if (g < G && n < N) {
-    h = s_star[g * N + n];
-    int qmin = 7, qmax = -8;
-    if (packed) {
-      for (int64_t k = g * group; k < (g + 1) * group; ++k) {
-        const int q = ref_nibble(packed, K, N, k, n) - 8;
-        qmin = min(qmin, q);
-        qmax = max(qmax, q);
-      }
-    } else {
-      qmin = -8;
-      qmax = 7;
-    }
-    const __half s = __ushort_as_half(h);
-    const __half add = __float2half_rn(1152.0f);
-    const float r_a = __half2float(__hfma(__int2half_rn(qmin), s, add));
-    const float r_b = __half2float(__hfma(__int2half_rn(qmax), s, add));
-    const float lo = fminf(r_a, r_b), hi = fmaxf(r_a, r_b);
-    if (!(lo >= 1025.0f && hi <= 1279.0f)) atomicOr(flags, kStatNeedClamp);  // NaN fails too
-  }
-  out[((n / kTileN) * G_pad + g) * kTileN + (n % kTileN)] = h;
 }
 
 // --- exhaustive-test hooks for the device conversion functions --------------
@@ -300,28 +303,34 @@ extern "C" int qqq_dequantize(const int8_t* codes, int64_t K, int64_t N, int64_t
   return ok();
 }
 
-extern "C" size_t qqq_repacked_weight_bytes(int mode, int64_t K, int64_t N) {
+extern "C" size_t qqq_repacked_weight_bytes(int mode, int64_t K, int64_t N, int64_t group) {
+  if (K <= 0 || N <= 0) return 0;
+  if (mode == kModePG && !pg_group_ok(group)) return 0;
   const int64_t kp = round_up(K, kKPadTo), np = round_up(N, kTileN);
-  return (size_t)(mode == kModeI8 ? kp * np : kp * np / 2);
+  return (size_t)((np / kTileN) * (kp / kSuperK) * ss_bytes(mode, group));
 }
 
-extern "C" size_t qqq_repacked_scale_bytes(int64_t K, int64_t N, int64_t group) {
-  if (group <= 0) return 0;
-  const int64_t kp = round_up(K, kKPadTo), np = round_up(N, kTileN);
-  return (size_t)(np * ((kp + group - 1) / group) * 2);
-}
-
-// mode PC / PG: nibble repack of the reference packed bytes.
-extern "C" int qqq_repack_weights(const uint8_t* packed, int64_t K, int64_t N, int mode, void* out, cudaStream_t st) {
+// PC / PG blob from the reference pack_i4 bytes (+ s* for PG). For PG,
+// flags_dev gets QQQ_STAT_NEED_CLAMP if the clamp-free converter would not be
+// bit-exact for these weights (the caller then uses the I8 blob instead).
+extern "C" int qqq_repack_weights(const uint8_t* packed, const uint16_t* s_star, int64_t K, int64_t N, int mode,
+                                  int64_t group, void* out, int32_t* flags_dev, cudaStream_t st) {
   if (K <= 0 || N <= 0) return kErrShape;
   if (mode != kModePC && mode != kModePG) return kErrConfig;
-  const int64_t np = round_up(N, kTileN), slabs = round_up(K, kKPadTo) / kSlabK;
+  if (mode == kModePG && (!pg_group_ok(group) || !s_star || !flags_dev || K % group != 0)) return kErrConfig;
+  const int64_t np = round_up(N, kTileN), kp = round_up(K, kKPadTo);
+  const int64_t slabs = kp / kSlabK, sspt = kp / kSuperK;
+  const int64_t ssb = ss_bytes(mode, group);
   dim3 grid(nblk(np, 128), (unsigned)slabs);
-  repack4_kernel<<<grid, 128, 0, st>>>(packed, K, N, np, slabs, mode, (uint8_t*)out);
+  repack4_kernel<<<grid, 128, 0, st>>>(packed, K, N, np, slabs, mode, ssb, (uint8_t*)out);
+  if (mode == kModePG) {
+    dim3 g2(nblk(np, 128), (unsigned)(sspt * pg_groups_per_ss(group)));
+    repack_scales_kernel<<<g2, 128, 0, st>>>(s_star, packed, K, N, np, group, ssb, sspt, (uint8_t*)out, flags_dev);
+  }
   return ok();
 }
 
-// mode I8 from an int8 K x N matrix (w8 != NULL) or from packed + s* (per-group,
+// I8 blob from an int8 K x N matrix (w8 != NULL) or from packed + s* (per-group,
 // exact scalar conversion incl. the clamp).
 extern "C" int qqq_repack_weights_i8(const int8_t* w8, const uint8_t* packed, const uint16_t* s_star, int64_t group,
                                      int64_t K, int64_t N, void* out, cudaStream_t st) {
@@ -330,17 +339,6 @@ extern "C" int qqq_repack_weights_i8(const int8_t* w8, const uint8_t* packed, co
   const int64_t np = round_up(N, kTileN), slabs = round_up(K, kKPadTo) / kSlabK;
   dim3 grid(nblk(np, 128), (unsigned)(slabs * 2));
   repack8_kernel<<<grid, 128, 0, st>>>(w8, packed, s_star, group, K, N, np, slabs, (uint8_t*)out);
-  return ok();
-}
-
-extern "C" int qqq_repack_scales(const uint16_t* s_star, const uint8_t* packed, int64_t K, int64_t N, int64_t group,
-                                 void* out, int32_t* flags_dev, cudaStream_t st) {
-  if (K <= 0 || N <= 0 || group <= 0 || K % group != 0) return kErrConfig;
-  const int64_t np = round_up(N, kTileN), kp = round_up(K, kKPadTo);
-  const int64_t gpad = (kp + group - 1) / group;
-  dim3 grid(nblk(np, 128), (unsigned)gpad);
-  repack_scales_kernel<<<grid, 128, 0, st>>>(s_star, packed, K, group, K / group, N, np, gpad, (uint16_t*)out,
-                                             flags_dev);
   return ok();
 }
 

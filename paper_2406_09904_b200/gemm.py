@@ -110,22 +110,9 @@ def _version_key(t: torch.Tensor):
     return (t.data_ptr(), t._version, tuple(t.shape))
 
 
-def _repacked_nibbles(qw: QuantizedWeights, mode: int) -> torch.Tensor:
-    packed = as_cuda(qw.packed, torch.uint8).contiguous()
-    key = ("w4", mode, _version_key(qw.packed))
-    hit = qw._cache.get("w4")
-    if hit is not None and hit[0] == key:
-        return hit[1]
-    dev = packed.device
-    lib = _lib.lib_for_device(dev)
-    k, n = qw.rows, qw.cols
-    if packed.shape != ((k + 1) // 2, n):
-        raise CorruptionError(f"packed shape {tuple(packed.shape)} inconsistent with K={k}, N={n}")
-    out = torch.empty(lib.qqq_repacked_weight_bytes(mode, k, n), dtype=torch.uint8, device=dev)
-    _lib.check(lib.qqq_repack_weights(_lib.ptr(packed), k, n, mode, _lib.ptr(out), _lib.stream_of(dev)),
-               "repack_weights")
-    qw._cache["w4"] = (key, out)
-    return out
+def _pg_fast_ok(g: int) -> bool:
+    """Per-group group sizes the nibble kernel layout supports (qqq_layout.cuh)."""
+    return g > 0 and ((g % 32 == 0 and 128 % g == 0) or g % 128 == 0)
 
 
 def _check_padding(qw: QuantizedWeights) -> None:
@@ -148,49 +135,63 @@ class PreparedWeights:
 
 
 def prepare(qw: QuantizedWeights, fused: FusedScales) -> PreparedWeights:
-    """One-time repack (cached) of the reference packing into the tcgen05 layout."""
-    dev_t = as_cuda(qw.packed)
-    dev = dev_t.device
+    """One-time repack (cached) of the reference packing into the tcgen05 blob.
+
+    Cache key: the identity and in-place version of qw.packed (and fused.s_star),
+    so a mutated or replaced tensor is repacked again.
+    """
+    packed = as_cuda(qw.packed, torch.uint8).contiguous()
+    dev = packed.device
     lib = _lib.lib_for_device(dev)
     k, n = qw.rows, qw.cols
+    if packed.shape != ((k + 1) // 2, n):
+        raise CorruptionError(f"packed shape {tuple(packed.shape)} inconsistent with K={k}, N={n}")
     if qw.scheme == PER_CHANNEL:
-        w = _repacked_nibbles(qw, _lib.MODE_PC)
-        return PreparedWeights(_lib.MODE_PC, w, None, 0, as_cuda(fused.s_w_folded, torch.float64).contiguous())
+        key = ("pc", _version_key(qw.packed))
+        hit = qw._cache.get("pc")
+        if hit is None or hit[0] != key:
+            w = torch.empty(lib.qqq_repacked_weight_bytes(_lib.MODE_PC, k, n, 0), dtype=torch.uint8, device=dev)
+            _lib.check(lib.qqq_repack_weights(_lib.ptr(packed), None, k, n, _lib.MODE_PC, 0, _lib.ptr(w), None,
+                                              _lib.stream_of(dev)), "repack_weights")
+            hit = (key, w)
+            qw._cache["pc"] = hit
+        return PreparedWeights(_lib.MODE_PC, hit[1], None, 0, as_cuda(fused.s_w_folded, torch.float64).contiguous())
     g = qw.group_size
     s_star = as_cuda(fused.s_star, torch.float16).contiguous()
     key = ("pg", _version_key(qw.packed), _version_key(fused.s_star), g)
     hit = fused._cache.get("pg")
     if hit is not None and hit[0] == key:
         return hit[1]
-    fast_ok = g % 256 == 0 or (g <= 128 and 128 % g == 0 and g % 32 == 0)
-    sc = None
-    if fast_ok:
-        sc = torch.empty(lib.qqq_repacked_scale_bytes(k, n, g) // 2, dtype=torch.float16, device=dev)
+    s_wc = as_cuda(fused.s_wc, torch.float64).contiguous()
+    prep = None
+    if _pg_fast_ok(g):
+        w = torch.empty(lib.qqq_repacked_weight_bytes(_lib.MODE_PG, k, n, g), dtype=torch.uint8, device=dev)
         flags = torch.zeros(1, dtype=torch.int32, device=dev)
-        packed = as_cuda(qw.packed, torch.uint8).contiguous()
-        _lib.check(lib.qqq_repack_scales(_lib.ptr(s_star), _lib.ptr(packed), k, n, g, _lib.ptr(sc), _lib.ptr(flags),
-                                         _lib.stream_of(dev)), "repack_scales")
-        fast_ok = (int(flags.item()) & _lib.STAT_NEED_CLAMP) == 0
-    if fast_ok:
-        prep = PreparedWeights(_lib.MODE_PG, _repacked_nibbles(qw, _lib.MODE_PG), sc, g,
-                               as_cuda(fused.s_wc, torch.float64).contiguous())
-    else:
+        _lib.check(lib.qqq_repack_weights(_lib.ptr(packed), _lib.ptr(s_star), k, n, _lib.MODE_PG, g, _lib.ptr(w),
+                                          _lib.ptr(flags), _lib.stream_of(dev)), "repack_weights")
+        if (int(flags.item()) & _lib.STAT_NEED_CLAMP) == 0:
+            prep = PreparedWeights(_lib.MODE_PG, w, None, g, s_wc)
+    if prep is None:
         # exact scalar FusedDequantQuant (with the reference clamp) into int8 once
-        packed = as_cuda(qw.packed, torch.uint8).contiguous()
-        w8 = torch.empty(lib.qqq_repacked_weight_bytes(_lib.MODE_I8, k, n), dtype=torch.uint8, device=dev)
+        w8 = torch.empty(lib.qqq_repacked_weight_bytes(_lib.MODE_I8, k, n, 0), dtype=torch.uint8, device=dev)
         _lib.check(lib.qqq_repack_weights_i8(None, _lib.ptr(packed), _lib.ptr(s_star), g, k, n, _lib.ptr(w8),
                                              _lib.stream_of(dev)), "repack_weights_i8")
-        prep = PreparedWeights(_lib.MODE_I8, w8, None, 0, as_cuda(fused.s_wc, torch.float64).contiguous())
+        prep = PreparedWeights(_lib.MODE_I8, w8, None, 0, s_wc)
     fused._cache["pg"] = (key, prep)
     return prep
 
 
 def _aligned_q(aq: QuantizedActivations) -> torch.Tensor:
+    """The kernel reads rows as 128-byte atoms: row pitch % 16 == 0 and >= round_up(K, 128)."""
     q = as_cuda(aq.q, torch.int8)
-    if q.stride(1) == 1 and q.stride(0) % 16 == 0 and q.data_ptr() % 16 == 0:
-        return q
     m, k = q.shape
-    kp = (k + 15) // 16 * 16
+    kp = (k + 127) // 128 * 128
+    if m == 0:
+        return q
+    pitch = q.stride(0) if m > 1 else kp
+    if (q.stride(1) == 1 and q.data_ptr() % 16 == 0 and pitch % 16 == 0 and pitch >= kp
+            and q.untyped_storage().nbytes() - q.storage_offset() >= (m - 1) * pitch + kp):
+        return q
     buf = torch.zeros((m, kp), dtype=torch.int8, device=q.device)
     buf[:, :k] = q
     return buf[:, :k]
@@ -219,8 +220,9 @@ def run_gemm(aq: QuantizedActivations, prep: PreparedWeights, n: int, with_acc: 
         dbg = cfg.get("dbg")
         c = _lib.GemmConfig(int(cfg.get("ntok", 0)), int(cfg.get("grid", 0)), int(cfg.get("split", -1)),
                             None if dbg is None else dbg.data_ptr())
-    rc = lib.qqq_w4a8_gemm_ex(prep.mode, _lib.ptr(q), q.stride(0), _lib.ptr(s_a), _lib.ptr(prep.w),
-                              _lib.ptr(prep.sc), prep.group, _lib.ptr(prep.s_col), m, n, k, _lib.ptr(y), y.stride(0),
+    ldq = q.stride(0) if m > 1 else (k + 127) // 128 * 128
+    rc = lib.qqq_w4a8_gemm_ex(prep.mode, _lib.ptr(q), ldq, _lib.ptr(s_a), _lib.ptr(prep.w),
+                              prep.group, _lib.ptr(prep.s_col), m, n, k, _lib.ptr(y), y.stride(0),
                               _lib.ptr(acc), n, _lib.ptr(ws), ws.numel(),
                               None if c is None else c, _lib.stream_of(dev))
     _lib.check(rc, "w4a8_gemm")
@@ -271,7 +273,7 @@ def gemm_i8_i32(aq, w8) -> torch.Tensor:
     dev = a.device
     lib = _lib.lib_for_device(dev)
     b = b.contiguous()
-    wb = torch.empty(lib.qqq_repacked_weight_bytes(_lib.MODE_I8, k, n), dtype=torch.uint8, device=dev)
+    wb = torch.empty(lib.qqq_repacked_weight_bytes(_lib.MODE_I8, k, n, 0), dtype=torch.uint8, device=dev)
     _lib.check(lib.qqq_repack_weights_i8(_lib.ptr(b), None, None, 0, k, n, _lib.ptr(wb), _lib.stream_of(dev)),
                "repack_weights_i8")
     ones = torch.ones(max(m, 1), dtype=torch.float64, device=dev)
@@ -282,8 +284,9 @@ def gemm_i8_i32(aq, w8) -> torch.Tensor:
     if m == 0:
         return acc
     ws = workspace(dev, lib.qqq_gemm_workspace_bytes(m, n, k))
-    _lib.check(lib.qqq_w4a8_gemm_ex(_lib.MODE_I8, _lib.ptr(q), q.stride(0), _lib.ptr(aqq.s_a), _lib.ptr(prep.w),
-                                    None, 0, None, m, n, k, None, n, _lib.ptr(acc), n, _lib.ptr(ws), ws.numel(), None,
+    ldq = q.stride(0) if m > 1 else (k + 127) // 128 * 128
+    _lib.check(lib.qqq_w4a8_gemm_ex(_lib.MODE_I8, _lib.ptr(q), ldq, _lib.ptr(aqq.s_a), _lib.ptr(prep.w),
+                                    0, None, m, n, k, None, n, _lib.ptr(acc), n, _lib.ptr(ws), ws.numel(), None,
                                     _lib.stream_of(dev)), "gemm_i8_i32")
     return acc
 

@@ -130,7 +130,7 @@ def quant_act_per_token(x, check: bool = True) -> QuantizedActivations:
     ldx = xt.stride(0) if m > 1 else k
     dev = xt.device
     lib = _lib.lib_for_device(dev)
-    kp = (k + 15) // 16 * 16  # 16-byte row pitch for the GEMM's TMA; view is M x K
+    kp = (k + 127) // 128 * 128  # row pitch = whole 128-byte atoms for the GEMM's TMA; view is M x K
     qbuf = torch.empty((m, kp), dtype=torch.int8, device=dev)
     s_a = torch.empty((m,), dtype=torch.float64, device=dev)
     status = _status(dev)
