@@ -36,14 +36,15 @@
 
 namespace qqq {
 
-constexpr int kNumThreads = 512;
-constexpr int kConvWarp0 = 0, kNumConvWarps = 8;
-constexpr int kEpiWarp0 = 8, kNumEpiWarps = 4;
-constexpr int kAllocWarp = 12;
-constexpr int kProducerWarp = 14;
-constexpr int kMmaWarp = 15;
+constexpr int kNumConvWarps = 16;
+constexpr int kConvWarp0 = 0;
+constexpr int kEpiWarp0 = kNumConvWarps, kNumEpiWarps = 4;
+constexpr int kAllocWarp = kEpiWarp0 + 4;
+constexpr int kProducerWarp = kEpiWarp0 + 6;
+constexpr int kMmaWarp = kEpiWarp0 + 7;
+constexpr int kNumThreads = (kMmaWarp + 1) * 32;
 constexpr int kSmemBudget = 225 * 1024;
-constexpr int kDbgSlots = 64;
+constexpr int kDbgSlots = 128;
 
 struct GemmParams {
   const uint8_t* w;     // repacked weight blob (qqq_layout.cuh)
@@ -329,30 +330,37 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(4 + it);
           const int b = it % C::kABufs;
           mbar_wait(&a_empty[b], ((it / C::kABufs) & 1) ^ 1);
+          if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(64 + it);
           const uint8_t* wst = smem + C::kOffW + s * C::kWBytes;
           uint8_t* abuf = smem + C::kOffA + b * C::kABytes;
+          constexpr int kUnits = BK / 8 / kNumConvWarps;  // warp-units: 32 rows x one 32-k slab
+          uint4 v[kUnits];
 #pragma unroll
-          for (int i = 0; i < BK / 64; ++i) {
-            const int wu = cw + i * kNumConvWarps;  // warp-unit: 32 rows x one 32-k slab
-            const int c = wu >> 2;                  // slab within the k-block
+          for (int i = 0; i < kUnits; ++i) {  // all shared loads first (ILP)
+            const int wu = cw + i * kNumConvWarps;
+            const int c = wu >> 2, row = ((wu & 3) << 5) + lane;
+            v[i] = *reinterpret_cast<const uint4*>(wst + (c >> 2) * p.ss_bytes + ((c & 3) * 128 + row) * 16);
+          }
+#pragma unroll
+          for (int i = 0; i < kUnits; ++i) {
+            const int wu = cw + i * kNumConvWarps;
+            const int c = wu >> 2;                   // slab within the k-block
             const int row = ((wu & 3) << 5) + lane;  // channel within the tile
-            const uint8_t* ssp = wst + (c >> 2) * p.ss_bytes;
-            const uint4 v = *reinterpret_cast<const uint4*>(ssp + ((c & 3) * 128 + row) * 16);
             uint4 o0, o1;
             if constexpr (MODE == kModePC) {
-              pc_convert_word(v.x, o0.x, o1.x);
-              pc_convert_word(v.y, o0.y, o1.y);
-              pc_convert_word(v.z, o0.z, o1.z);
-              pc_convert_word(v.w, o0.w, o1.w);
+              pc_convert_word(v[i].x, o0.x, o1.x);
+              pc_convert_word(v[i].y, o0.y, o1.y);
+              pc_convert_word(v[i].z, o0.z, o1.z);
+              pc_convert_word(v[i].w, o0.w, o1.w);
             } else {
               const int lg = ((c & 3) * 32) / geff;
-              const __half s1 = reinterpret_cast<const __half*>(ssp + 8192)[lg * 128 + row];
+              const __half s1 = reinterpret_cast<const __half*>(wst + (c >> 2) * p.ss_bytes + 8192)[lg * 128 + row];
               const __half2 s2 = __halves2half2(s1, s1);
               const __half2 s16 = __hmul2(s2, u32_as_h2(0x2C002C00u));  // * 1/16
-              pg_convert_word<false>(v.x, s2, s16, o0.x, o0.y);
-              pg_convert_word<false>(v.y, s2, s16, o0.z, o0.w);
-              pg_convert_word<false>(v.z, s2, s16, o1.x, o1.y);
-              pg_convert_word<false>(v.w, s2, s16, o1.z, o1.w);
+              pg_convert_word<false>(v[i].x, s2, s16, o0.x, o0.y);
+              pg_convert_word<false>(v[i].y, s2, s16, o0.z, o0.w);
+              pg_convert_word<false>(v[i].z, s2, s16, o1.x, o1.y);
+              pg_convert_word<false>(v[i].w, s2, s16, o1.z, o1.w);
             }
             *reinterpret_cast<uint4*>(abuf + ((2 * c) * 128 + row) * 16) = o0;
             *reinterpret_cast<uint4*>(abuf + ((2 * c + 1) * 128 + row) * 16) = o1;
@@ -363,6 +371,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             mbar_arrive(&a_full[b]);
             mbar_arrive(&empty[s]);
           }
+          if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(80 + it);
         }
       }
     }
@@ -410,6 +419,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[j]);
         }
+        if (lead && seg == 0 && c < 16) QQQ_STAMP(44 + c);
         if (whole) {
           store_outputs(p, r, tok0 + c0, tvalid - c0, n, n_ok, s_col);
         } else {

@@ -12,6 +12,10 @@ NAMES = {0: "start", 1: "setup", 2: "w_issued", 3: "dep_wait", 63: "end"}
 for i in range(16):
     NAMES[4 + i] = f"full{i}"
     NAMES[20 + i] = f"mma{i}"
+for c in range(16):
+    NAMES[44 + c] = f"epi0_c{c}"
+    NAMES[64 + c] = f"conv_ae{c}"
+    NAMES[80 + c] = f"conv_done{c}"
 for sg in range(4):
     NAMES[36 + 2 * sg] = f"accfull{sg}"
     NAMES[37 + 2 * sg] = f"epi_done{sg}"
@@ -30,7 +34,7 @@ aq = Q.quant_act_per_token(x)
 y = torch.empty((a.m, n), dtype=torch.float16, device=dev)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 for rep in range(3):
-    dbg = torch.zeros((1024, 64), dtype=torch.int64, device=dev)
+    dbg = torch.zeros((1024, 128), dtype=torch.int64, device=dev)
     cfg = dict(json.loads(a.cfg), dbg=dbg)
     flush.zero_()
     torch.cuda.synchronize()
@@ -41,7 +45,8 @@ ctas = d[:, 0] > 0
 d = d[ctas]
 t0 = d[:, 0].min()
 print(f"{a.shape} M={a.m} {a.scheme} cfg={a.cfg} ctas={int(ctas.sum())}  (us relative to first CTA start)")
-for slot in sorted(NAMES):
+order = sorted(NAMES, key=lambda sl: (sl >= 4 and sl < 20 or sl >= 64, sl))
+for slot in sorted(NAMES, key=lambda sl: ({20: 1}.get(sl // 16 * 16, 0), sl)):
     col = d[:, slot]
     v = col[col > 0]
     if v.size == 0:
