@@ -36,11 +36,12 @@
 
 namespace qqq {
 
-constexpr int kNumConvWarps = 16;
+constexpr int kNumConvWarps = 8;
 constexpr int kConvWarp0 = 0;
 constexpr int kEpiWarp0 = kNumConvWarps, kNumEpiWarps = 4;
 constexpr int kAllocWarp = kEpiWarp0 + 4;
-constexpr int kProducerWarp = kEpiWarp0 + 6;
+constexpr int kActProducerWarp = kEpiWarp0 + 5;
+constexpr int kWProducerWarp = kEpiWarp0 + 6;
 constexpr int kMmaWarp = kEpiWarp0 + 7;
 constexpr int kNumThreads = (kMmaWarp + 1) * 32;
 constexpr int kSmemBudget = 225 * 1024;
@@ -66,22 +67,27 @@ struct GemmParams {
 template <int MODE, int NTOK, int BK>
 struct Cfg {
   static constexpr bool kConvert = MODE != kModeI8;
-  static constexpr int kActBytes = NTOK * BK;
-  // worst-case super-slab bytes (PG with g = 32) for the smem carve-up
+  // two independent TMA rings: weights (released by the converters right after
+  // their shared-memory loads, or by the MMA in I8 mode) and activations
+  // (released by the MMA)
+  static constexpr int kXBytes = NTOK * BK;
   static constexpr int kSSMax = MODE == kModeI8 ? 16384 : MODE == kModePC ? 8192 : 8192 + 256 * 4;
-  static constexpr int kWBytes = (BK / 128) * kSSMax;
+  static constexpr int kWBytes = (BK / 128) * kSSMax;  // worst case (PG, g = 32)
   static constexpr int kABytes = BK * 128;
   static constexpr int kABufs = kConvert ? 2 : 0;
-  static constexpr int kStageBytes = kActBytes + kWBytes;
-  static constexpr int kStagesRaw = (kSmemBudget - 4096 - kABufs * kABytes) / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static_assert(kStages >= 2, "shared memory budget too small");
-  static constexpr int kOffAct = 0;  // 1024-aligned: NTOK*BK is a multiple of 2048
-  static constexpr int kOffW = kOffAct + kStages * kActBytes;
-  static constexpr int kOffA = (kOffW + kStages * kWBytes + 1023) / 1024 * 1024;
+  static constexpr int kRingBudget = kSmemBudget - 4096 - kABufs * kABytes;
+  static constexpr int kXStagesRaw = (kRingBudget / 4) / kXBytes;  // ~1/4 of the rings to activations
+  static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > 8 ? 8 : kXStagesRaw);
+  static constexpr int kWStagesRaw = (kRingBudget - kXStages * kXBytes) / kWBytes;
+  static constexpr int kWStages = kWStagesRaw > 12 ? 12 : kWStagesRaw;
+  static_assert(kWStages >= 2, "shared memory budget too small");
+  static constexpr int kOffX = 0;  // 1024-aligned: NTOK*BK is a multiple of 2048
+  static constexpr int kOffW = kOffX + kXStages * kXBytes;
+  static constexpr int kOffA = (kOffW + kWStages * kWBytes + 1023) / 1024 * 1024;
   static constexpr int kOffBar = kOffA + kABufs * kABytes;
-  static constexpr int kNumBars = 2 * kStages + 2 * kABufs + 4;
+  static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 2 * kABufs + 4;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // +1024 alignment slack
+  static_assert(kSmemBytes <= 227 * 1024, "over the per-CTA shared memory limit");
   static constexpr uint32_t kTmemCols = (2 * NTOK <= 32) ? 32 : (2 * NTOK <= 64) ? 64 : (2 * NTOK <= 128) ? 128
                                         : (2 * NTOK <= 256) ? 256 : 512;
   static constexpr uint32_t kIdesc = make_idesc_i8(128, NTOK);
@@ -191,9 +197,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + C::kStages;
-  uint64_t* a_full = bars + 2 * C::kStages;
+  uint64_t* x_full = bars;
+  uint64_t* x_empty = x_full + C::kXStages;
+  uint64_t* w_full = x_empty + C::kXStages;
+  uint64_t* w_empty = w_full + C::kWStages;
+  uint64_t* a_full = w_empty + C::kWStages;
   uint64_t* a_empty = a_full + C::kABufs;
   uint64_t* acc_full = a_empty + C::kABufs;
   uint64_t* acc_empty = acc_full + 2;
@@ -206,9 +214,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   if (threadIdx.x == 0) {
     QQQ_STAMP(0);
     griddep_launch_dependents();
-    for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::kConvert ? kNumConvWarps + 1 : 1);
+    for (int s = 0; s < C::kXStages; ++s) {
+      mbar_init(&x_full[s], 1);
+      mbar_init(&x_empty[s], 1);
+    }
+    for (int s = 0; s < C::kWStages; ++s) {
+      mbar_init(&w_full[s], 1);
+      mbar_init(&w_empty[s], C::kConvert ? kNumConvWarps : 1);
     }
     for (int b = 0; b < C::kABufs; ++b) {
       mbar_init(&a_full[b], kNumConvWarps);
@@ -220,53 +232,50 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     mbar_fence_init();
   }
-  if (warp == kProducerWarp && lane == 0) tma_prefetch_desc(&act_map);
+  if (warp == kActProducerWarp && lane == 0) tma_prefetch_desc(&act_map);
   if (warp == kAllocWarp) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int wbytes = (BK / 128) * p.ss_bytes;  // this launch's weight bytes per k-block
-  const uint32_t stage_tx = (uint32_t)(C::kActBytes + wbytes);
 
-  if (warp == kProducerWarp) {
-    // ======================= TMA / bulk producer =======================
+  if (warp == kWProducerWarp) {
+    // ===================== weight producer (bulk copies) =====================
+    // Weights never depend on the previous kernel in the stream: no PDL wait,
+    // so under PDL they stream in while the previous kernel drains.
     if (lane == 0) {
       QQQ_STAMP(1);
-      auto issue_weights = [&](int n_tile, int kb, int s) {
-        const int64_t ss0 = (int64_t)n_tile * p.ss_per_tile + (int64_t)kb * (BK / 128);
-        bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &full[s]);
-      };
-      int tile, kb0, kb1;
-      // pass 1: weights do not depend on the previous kernel -> stream them
-      // into the first kStages stages before the PDL grid-dependency wait
-      uint32_t pre = 0;
-      {
-        SegIter si = make_iter(p);
-        while (pre < (uint32_t)C::kStages && si.next(tile, kb0, kb1)) {
-          for (int kb = kb0; kb < kb1 && pre < (uint32_t)C::kStages; ++kb, ++pre) {
-            mbar_arrive_expect_tx(&full[pre], stage_tx);
-            issue_weights(tile / p.tok_tiles, kb, pre);
-          }
-        }
-      }
-      QQQ_STAMP(2);
-      griddep_wait();
-      QQQ_STAMP(3);
-      // pass 2: activations for the pre-armed stages, then the steady-state ring
+      const uint32_t wbytes = (uint32_t)((BK / 128) * p.ss_bytes);
       SegIter si = make_iter(p);
+      int tile, kb0, kb1;
       uint32_t it = 0;
       while (si.next(tile, kb0, kb1)) {
         const int n_tile = tile / p.tok_tiles;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % C::kWStages;
+          mbar_wait(&w_empty[s], ((it / C::kWStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&w_full[s], wbytes);
+          const int64_t ss0 = (int64_t)n_tile * p.ss_per_tile + (int64_t)kb * (BK / 128);
+          bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &w_full[s]);
+        }
+      }
+      QQQ_STAMP(2);
+    }
+  } else if (warp == kActProducerWarp) {
+    // ================== activation producer (3-D tensor TMA) ==================
+    if (lane == 0) {
+      griddep_wait();  // the int8 activations come from the previous kernel
+      QQQ_STAMP(3);
+      SegIter si = make_iter(p);
+      int tile, kb0, kb1;
+      uint32_t it = 0;
+      while (si.next(tile, kb0, kb1)) {
         const int tok0 = (tile % p.tok_tiles) * NTOK;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % C::kStages;
-          if (it >= pre) {
-            mbar_wait(&empty[s], ((it / C::kStages) & 1) ^ 1);
-            mbar_arrive_expect_tx(&full[s], stage_tx);
-            issue_weights(n_tile, kb, s);
-          }
-          tma_load_3d(smem + C::kOffAct + s * C::kActBytes, &act_map, 0, tok0, kb * (BK / 128), &full[s]);
+          const int s = it % C::kXStages;
+          mbar_wait(&x_empty[s], ((it / C::kXStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&x_full[s], C::kXBytes);
+          tma_load_3d(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0, kb * (BK / 128), &x_full[s]);
         }
       }
     }
@@ -275,26 +284,28 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (lane == 0) {
       SegIter si = make_iter(p);
       int tile, kb0, kb1;
-      uint32_t it = 0, ait = 0, seg = 0;
+      uint32_t it = 0, seg = 0;
       while (si.next(tile, kb0, kb1)) {
         const int j = seg & 1;
         mbar_wait(&acc_empty[j], ((seg >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + j * NTOK;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % C::kStages;
-          mbar_wait(&full[s], (it / C::kStages) & 1);
+          const int xs = it % C::kXStages;
+          mbar_wait(&x_full[xs], (it / C::kXStages) & 1);
           uint32_t a_addr;
-          int b = 0;
+          int b = 0, ws = 0;
           if constexpr (C::kConvert) {
-            b = ait % C::kABufs;
-            mbar_wait(&a_full[b], (ait / C::kABufs) & 1);
+            b = it % C::kABufs;
+            mbar_wait(&a_full[b], (it / C::kABufs) & 1);
             a_addr = smem_u32(smem + C::kOffA + b * C::kABytes);
           } else {
-            a_addr = smem_u32(smem + C::kOffW + s * C::kWBytes);
+            ws = it % C::kWStages;
+            mbar_wait(&w_full[ws], (it / C::kWStages) & 1);
+            a_addr = smem_u32(smem + C::kOffW + ws * C::kWBytes);
           }
           tc_fence_after();
-          const uint32_t act_addr = smem_u32(smem + C::kOffAct + s * C::kActBytes);
+          const uint32_t act_addr = smem_u32(smem + C::kOffX + xs * C::kXBytes);
 #pragma unroll
           for (int kk = 0; kk < BK / 32; ++kk) {
             // A: canonical K-major, no swizzle: [k16 chunk][128 rows][16 B]
@@ -304,11 +315,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const uint64_t b_desc = make_smem_desc(b_addr, 16, 1024, 2);
             mma_i8_ss(d_tmem, a_desc, b_desc, C::kIdesc, (kb > kb0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&empty[s]);
+          mma_commit(&x_empty[xs]);
           if (it < 16) QQQ_STAMP(20 + it);
           if constexpr (C::kConvert) {
             mma_commit(&a_empty[b]);
-            ++ait;
+          } else {
+            mma_commit(&w_empty[ws]);
           }
         }
         mma_commit(&acc_full[j]);
@@ -323,54 +335,58 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       SegIter si = make_iter(p);
       int tile, kb0, kb1;
       uint32_t it = 0;
+      constexpr int kUnits = BK / 8 / kNumConvWarps;  // warp-units: 32 rows x one 32-k slab
       while (si.next(tile, kb0, kb1)) {
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % C::kStages;
-          mbar_wait(&full[s], (it / C::kStages) & 1);
+          const int s = it % C::kWStages;
+          mbar_wait(&w_full[s], (it / C::kWStages) & 1);
           if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(4 + it);
-          const int b = it % C::kABufs;
-          mbar_wait(&a_empty[b], ((it / C::kABufs) & 1) ^ 1);
-          if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(64 + it);
           const uint8_t* wst = smem + C::kOffW + s * C::kWBytes;
-          uint8_t* abuf = smem + C::kOffA + b * C::kABytes;
-          constexpr int kUnits = BK / 8 / kNumConvWarps;  // warp-units: 32 rows x one 32-k slab
           uint4 v[kUnits];
+          __half s1[kUnits];
 #pragma unroll
           for (int i = 0; i < kUnits; ++i) {  // all shared loads first (ILP)
             const int wu = cw + i * kNumConvWarps;
             const int c = wu >> 2, row = ((wu & 3) << 5) + lane;
-            v[i] = *reinterpret_cast<const uint4*>(wst + (c >> 2) * p.ss_bytes + ((c & 3) * 128 + row) * 16);
+            const uint8_t* ssp = wst + (c >> 2) * p.ss_bytes;
+            v[i] = *reinterpret_cast<const uint4*>(ssp + ((c & 3) * 128 + row) * 16);
+            if constexpr (MODE == kModePG)
+              s1[i] = reinterpret_cast<const __half*>(ssp + 8192)[(((c & 3) * 32) / geff) * 128 + row];
           }
+          uint4 o[2 * kUnits];
+#pragma unroll
+          for (int i = 0; i < kUnits; ++i) {
+            if constexpr (MODE == kModePC) {
+              pc_convert_word(v[i].x, o[2 * i].x, o[2 * i + 1].x);
+              pc_convert_word(v[i].y, o[2 * i].y, o[2 * i + 1].y);
+              pc_convert_word(v[i].z, o[2 * i].z, o[2 * i + 1].z);
+              pc_convert_word(v[i].w, o[2 * i].w, o[2 * i + 1].w);
+            } else {
+              const __half2 s2 = __halves2half2(s1[i], s1[i]);
+              const __half2 s16 = __hmul2(s2, u32_as_h2(0x2C002C00u));  // * 1/16
+              pg_convert_word<false>(v[i].x, s2, s16, o[2 * i].x, o[2 * i].y);
+              pg_convert_word<false>(v[i].y, s2, s16, o[2 * i].z, o[2 * i].w);
+              pg_convert_word<false>(v[i].z, s2, s16, o[2 * i + 1].x, o[2 * i + 1].y);
+              pg_convert_word<false>(v[i].w, s2, s16, o[2 * i + 1].z, o[2 * i + 1].w);
+            }
+          }
+          // the packed stage is consumed (values are in registers): release it now
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&w_empty[s]);
+          const int b = it % C::kABufs;
+          mbar_wait(&a_empty[b], ((it / C::kABufs) & 1) ^ 1);
+          if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(64 + it);
+          uint8_t* abuf = smem + C::kOffA + b * C::kABytes;
 #pragma unroll
           for (int i = 0; i < kUnits; ++i) {
             const int wu = cw + i * kNumConvWarps;
-            const int c = wu >> 2;                   // slab within the k-block
-            const int row = ((wu & 3) << 5) + lane;  // channel within the tile
-            uint4 o0, o1;
-            if constexpr (MODE == kModePC) {
-              pc_convert_word(v[i].x, o0.x, o1.x);
-              pc_convert_word(v[i].y, o0.y, o1.y);
-              pc_convert_word(v[i].z, o0.z, o1.z);
-              pc_convert_word(v[i].w, o0.w, o1.w);
-            } else {
-              const int lg = ((c & 3) * 32) / geff;
-              const __half s1 = reinterpret_cast<const __half*>(wst + (c >> 2) * p.ss_bytes + 8192)[lg * 128 + row];
-              const __half2 s2 = __halves2half2(s1, s1);
-              const __half2 s16 = __hmul2(s2, u32_as_h2(0x2C002C00u));  // * 1/16
-              pg_convert_word<false>(v[i].x, s2, s16, o0.x, o0.y);
-              pg_convert_word<false>(v[i].y, s2, s16, o0.z, o0.w);
-              pg_convert_word<false>(v[i].z, s2, s16, o1.x, o1.y);
-              pg_convert_word<false>(v[i].w, s2, s16, o1.z, o1.w);
-            }
-            *reinterpret_cast<uint4*>(abuf + ((2 * c) * 128 + row) * 16) = o0;
-            *reinterpret_cast<uint4*>(abuf + ((2 * c + 1) * 128 + row) * 16) = o1;
+            const int c = wu >> 2, row = ((wu & 3) << 5) + lane;
+            *reinterpret_cast<uint4*>(abuf + ((2 * c) * 128 + row) * 16) = o[2 * i];
+            *reinterpret_cast<uint4*>(abuf + ((2 * c + 1) * 128 + row) * 16) = o[2 * i + 1];
           }
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&a_full[b]);
-            mbar_arrive(&empty[s]);
-          }
+          if (lane == 0) mbar_arrive(&a_full[b]);
           if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(80 + it);
         }
       }
