@@ -73,9 +73,15 @@ struct Cfg {
   static constexpr int kXBytes = NTOK * BK;
   static constexpr int kSSMax = MODE == kModeI8 ? 16384 : MODE == kModePC ? 8192 : 8192 + 256 * 4;
   static constexpr int kWBytes = (BK / 128) * kSSMax;  // worst case (PG, g = 32)
-  static constexpr int kABytes = BK * 128;
-  static constexpr int kABufs = kConvert ? 2 : 0;
-  static constexpr int kRingBudget = kSmemBudget - 4096 - kABufs * kABytes;
+  // Converted int8 weights (the MMA A operand) live in TMEM, not shared memory:
+  // kABufs buffers of BK/4 columns (128 lanes x 4 int8 per column). This keeps
+  // the 1 B/weight operand off the shared-memory crossbar, which otherwise
+  // bounds the decode stream (TMA write + STS + MMA read of every weight).
+  static constexpr int kABufs = kConvert ? 4 : 0;
+  static constexpr int kACols = BK / 4;
+  static constexpr int kAccBufs = NTOK == 256 ? 1 : 2;
+  static constexpr int kAccCols = kAccBufs * NTOK;
+  static constexpr int kRingBudget = kSmemBudget - 4096;
   static constexpr int kXStagesRaw = (kRingBudget / 4) / kXBytes;  // ~1/4 of the rings to activations
   static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > 8 ? 8 : kXStagesRaw);
   static constexpr int kWStagesRaw = (kRingBudget - kXStages * kXBytes) / kWBytes;
@@ -83,13 +89,14 @@ struct Cfg {
   static_assert(kWStages >= 2, "shared memory budget too small");
   static constexpr int kOffX = 0;  // 1024-aligned: NTOK*BK is a multiple of 2048
   static constexpr int kOffW = kOffX + kXStages * kXBytes;
-  static constexpr int kOffA = (kOffW + kWStages * kWBytes + 1023) / 1024 * 1024;
-  static constexpr int kOffBar = kOffA + kABufs * kABytes;
+  static constexpr int kOffBar = (kOffW + kWStages * kWBytes + 1023) / 1024 * 1024;
   static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 2 * kABufs + 4;
   static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // +1024 alignment slack
   static_assert(kSmemBytes <= 227 * 1024, "over the per-CTA shared memory limit");
-  static constexpr uint32_t kTmemCols = (2 * NTOK <= 32) ? 32 : (2 * NTOK <= 64) ? 64 : (2 * NTOK <= 128) ? 128
-                                        : (2 * NTOK <= 256) ? 256 : 512;
+  static constexpr int kTmemNeed = kAccCols + kABufs * kACols;
+  static_assert(kTmemNeed <= 512, "TMEM over-subscribed");
+  static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
+                                        : kTmemNeed <= 256 ? 256 : 512;
   static constexpr uint32_t kIdesc = make_idesc_i8(128, NTOK);
   static_assert(NTOK % 16 == 0 && NTOK >= 16 && NTOK <= 256, "invalid UMMA N");
   static_assert(BK % 128 == 0, "BK must be a multiple of the 128-byte swizzle atom");
@@ -226,7 +233,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       mbar_init(&a_full[b], kNumConvWarps);
       mbar_init(&a_empty[b], 1);
     }
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < C::kAccBufs; ++j) {
       mbar_init(&acc_full[j], 1);
       mbar_init(&acc_empty[j], kNumEpiWarps);
     }
@@ -286,8 +293,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       int tile, kb0, kb1;
       uint32_t it = 0, seg = 0;
       while (si.next(tile, kb0, kb1)) {
-        const int j = seg & 1;
-        mbar_wait(&acc_empty[j], ((seg >> 1) & 1) ^ 1);
+        const int j = seg % C::kAccBufs;
+        mbar_wait(&acc_empty[j], ((seg / C::kAccBufs) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + j * NTOK;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           if constexpr (C::kConvert) {
             b = it % C::kABufs;
             mbar_wait(&a_full[b], (it / C::kABufs) & 1);
-            a_addr = smem_u32(smem + C::kOffA + b * C::kABytes);
+            a_addr = tmem_base + C::kAccCols + b * C::kACols;  // TMEM column address
           } else {
             ws = it % C::kWStages;
             mbar_wait(&w_full[ws], (it / C::kWStages) & 1);
@@ -308,12 +315,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           const uint32_t act_addr = smem_u32(smem + C::kOffX + xs * C::kXBytes);
 #pragma unroll
           for (int kk = 0; kk < BK / 32; ++kk) {
-            // A: canonical K-major, no swizzle: [k16 chunk][128 rows][16 B]
-            const uint64_t a_desc = make_smem_desc(a_addr + kk * 2 * 2048, 2048, 128, 0);
             // B: SWIZZLE_128B [k-atom][NTOK rows][128 B]; 32 B K-steps inside the atom
             const uint32_t b_addr = act_addr + (kk / 4) * (NTOK * 128) + (kk % 4) * 32;
             const uint64_t b_desc = make_smem_desc(b_addr, 16, 1024, 2);
-            mma_i8_ss(d_tmem, a_desc, b_desc, C::kIdesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
+            if constexpr (C::kConvert) {
+              mma_i8_ts(d_tmem, a_addr + kk * 8, b_desc, C::kIdesc, acc);  // A: 8 TMEM columns per K=32
+            } else {
+              // A: canonical K-major, no swizzle: [k16 chunk][128 rows][16 B]
+              mma_i8_ss(d_tmem, make_smem_desc(a_addr + kk * 2 * 2048, 2048, 128, 0), b_desc, C::kIdesc, acc);
+            }
           }
           mma_commit(&x_empty[xs]);
           if (it < 16) QQQ_STAMP(20 + it);
@@ -329,45 +340,48 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
   } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kNumConvWarps) {
     // ====================== INT4 -> INT8 converters ======================
+    // Warp w owns TMEM lane quadrant q = w % 4 (rows 32q..32q+31) and every
+    // other 32-k slab (parity w / 4): thread = one output channel.
     if constexpr (C::kConvert) {
-      const int cw = warp - kConvWarp0;
+      const int q = warp & 3, h = (warp >> 2) & 1;
+      const int row = q * 32 + lane;
       const int geff = p.group < 128 ? p.group : 128;
+      const uint32_t a_lane = tmem_base + ((uint32_t)(q * 32) << 16) + C::kAccCols;
       SegIter si = make_iter(p);
       int tile, kb0, kb1;
       uint32_t it = 0;
-      constexpr int kUnits = BK / 8 / kNumConvWarps;  // warp-units: 32 rows x one 32-k slab
+      constexpr int kSlabs = BK / 32 / 2;  // slabs per warp per k-block
       while (si.next(tile, kb0, kb1)) {
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::kWStages;
           mbar_wait(&w_full[s], (it / C::kWStages) & 1);
-          if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(4 + it);
+          if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(4 + it);
           const uint8_t* wst = smem + C::kOffW + s * C::kWBytes;
-          uint4 v[kUnits];
-          __half s1[kUnits];
+          uint4 v[kSlabs];
+          __half s1[kSlabs];
 #pragma unroll
-          for (int i = 0; i < kUnits; ++i) {  // all shared loads first (ILP)
-            const int wu = cw + i * kNumConvWarps;
-            const int c = wu >> 2, row = ((wu & 3) << 5) + lane;
+          for (int i = 0; i < kSlabs; ++i) {  // all shared loads first (ILP)
+            const int c = h + 2 * i;
             const uint8_t* ssp = wst + (c >> 2) * p.ss_bytes;
             v[i] = *reinterpret_cast<const uint4*>(ssp + ((c & 3) * 128 + row) * 16);
             if constexpr (MODE == kModePG)
               s1[i] = reinterpret_cast<const __half*>(ssp + 8192)[(((c & 3) * 32) / geff) * 128 + row];
           }
-          uint4 o[2 * kUnits];
+          uint32_t o[kSlabs][8];
 #pragma unroll
-          for (int i = 0; i < kUnits; ++i) {
+          for (int i = 0; i < kSlabs; ++i) {
             if constexpr (MODE == kModePC) {
-              pc_convert_word(v[i].x, o[2 * i].x, o[2 * i + 1].x);
-              pc_convert_word(v[i].y, o[2 * i].y, o[2 * i + 1].y);
-              pc_convert_word(v[i].z, o[2 * i].z, o[2 * i + 1].z);
-              pc_convert_word(v[i].w, o[2 * i].w, o[2 * i + 1].w);
+              pc_convert_word(v[i].x, o[i][0], o[i][4]);
+              pc_convert_word(v[i].y, o[i][1], o[i][5]);
+              pc_convert_word(v[i].z, o[i][2], o[i][6]);
+              pc_convert_word(v[i].w, o[i][3], o[i][7]);
             } else {
               const __half2 s2 = __halves2half2(s1[i], s1[i]);
               const __half2 s16 = __hmul2(s2, u32_as_h2(0x2C002C00u));  // * 1/16
-              pg_convert_word<false>(v[i].x, s2, s16, o[2 * i].x, o[2 * i].y);
-              pg_convert_word<false>(v[i].y, s2, s16, o[2 * i].z, o[2 * i].w);
-              pg_convert_word<false>(v[i].z, s2, s16, o[2 * i + 1].x, o[2 * i + 1].y);
-              pg_convert_word<false>(v[i].w, s2, s16, o[2 * i + 1].z, o[2 * i + 1].w);
+              pg_convert_word<false>(v[i].x, s2, s16, o[i][0], o[i][1]);
+              pg_convert_word<false>(v[i].y, s2, s16, o[i][2], o[i][3]);
+              pg_convert_word<false>(v[i].z, s2, s16, o[i][4], o[i][5]);
+              pg_convert_word<false>(v[i].w, s2, s16, o[i][6], o[i][7]);
             }
           }
           // the packed stage is consumed (values are in registers): release it now
@@ -375,19 +389,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           if (lane == 0) mbar_arrive(&w_empty[s]);
           const int b = it % C::kABufs;
           mbar_wait(&a_empty[b], ((it / C::kABufs) & 1) ^ 1);
-          if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(64 + it);
-          uint8_t* abuf = smem + C::kOffA + b * C::kABytes;
+          tc_fence_after();
+          if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(64 + it);
 #pragma unroll
-          for (int i = 0; i < kUnits; ++i) {
-            const int wu = cw + i * kNumConvWarps;
-            const int c = wu >> 2, row = ((wu & 3) << 5) + lane;
-            *reinterpret_cast<uint4*>(abuf + ((2 * c) * 128 + row) * 16) = o[2 * i];
-            *reinterpret_cast<uint4*>(abuf + ((2 * c + 1) * 128 + row) * 16) = o[2 * i + 1];
-          }
-          fence_proxy_async_smem();
+          for (int i = 0; i < kSlabs; ++i) tmem_st8(a_lane + b * C::kACols + (h + 2 * i) * 8, o[i]);
+          tmem_wait_st();
+          tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_full[b]);
-          if (cw == 0 && lane == 0 && it < 16) QQQ_STAMP(80 + it);
+          if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(80 + it);
         }
       }
     }
@@ -401,8 +411,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     int tile, kb0, kb1;
     uint32_t seg = 0;
     while (si.next(tile, kb0, kb1)) {
-      const int j = seg & 1;
-      mbar_wait(&acc_full[j], (seg >> 1) & 1);
+      const int j = seg % C::kAccBufs;
+      mbar_wait(&acc_full[j], (seg / C::kAccBufs) & 1);
       tc_fence_after();
       if (lead && seg < 4) QQQ_STAMP(36 + 2 * seg);
       const int n_tile = tile / p.tok_tiles;
