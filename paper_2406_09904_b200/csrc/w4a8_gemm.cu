@@ -81,7 +81,7 @@ struct Cfg {
   static constexpr int kACols = BK / 4;
   static constexpr int kAccBufs = NTOK == 256 ? 1 : 2;
   static constexpr int kAccCols = kAccBufs * NTOK;
-  static constexpr int kRingBudget = kSmemBudget - 4096;
+  static constexpr int kRingBudget = kSmemBudget - 4096 - NTOK * 8;
   static constexpr int kXStagesRaw = (kRingBudget / 4) / kXBytes;  // ~1/4 of the rings to activations
   static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > 8 ? 8 : kXStagesRaw);
   static constexpr int kWStagesRaw = (kRingBudget - kXStages * kXBytes) / kWBytes;
@@ -91,7 +91,8 @@ struct Cfg {
   static constexpr int kOffW = kOffX + kXStages * kXBytes;
   static constexpr int kOffBar = (kOffW + kWStages * kWBytes + 1023) / 1024 * 1024;
   static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 2 * kABufs + 4;
-  static constexpr int kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // +1024 alignment slack
+  static constexpr int kOffSA = kOffBar + (kNumBars * 8 + 16 + 15) / 16 * 16;  // per-token scales of a tile (f64)
+  static constexpr int kSmemBytes = kOffSA + NTOK * 8 + 1024;                // +1024 alignment slack
   static_assert(kSmemBytes <= 227 * 1024, "over the per-CTA shared memory limit");
   static constexpr int kTmemNeed = kAccCols + kABufs * kACols;
   static_assert(kTmemNeed <= 512, "TMEM over-subscribed");
@@ -139,12 +140,9 @@ QQQ_DEVICE void tma_load_3d(void* smem_dst, const CUtensorMap* map, int32_t c0, 
 // Dequant epilogue for up to 16 consecutive tokens of one output channel n:
 // y = f16((acc * s_a[t]) * s_col[n]) in f64 with one final RN rounding
 // (gemm.py:182-184 / 200-202); acc written as-is when requested.
-QQQ_DEVICE void store_outputs(const GemmParams& p, const uint32_t (&r)[16], int t0, int nvalid, int n, bool n_ok,
-                              double s_col) {
+QQQ_DEVICE void store_outputs(const GemmParams& p, const uint32_t (&r)[16], const double* sa, int t0, int nvalid,
+                              int n, bool n_ok, double s_col) {
   if (!n_ok) return;
-  double sa[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) sa[i] = (i < nvalid) ? __ldg(p.s_a + t0 + i) : 0.0;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     if (i < nvalid) {
@@ -213,7 +211,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* acc_full = a_empty + C::kABufs;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
-  volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -403,85 +400,107 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpiWarps) {
     // ============================== epilogue ==============================
+    // Whole tiles go straight from TMEM to y. A tile split over CTAs
+    // b_first..b_last (stream-K) is finished by its OWNER b_first, for which it
+    // is the last segment of its range; the other CTAs handle it first in
+    // theirs, store their int32 partial to a workspace slot and release an
+    // arrival counter. The owner acquires the counter, adds the partials to its
+    // own TMEM accumulator (exact integer sum) and applies the dequant. All
+    // CTAs of the grid are co-resident (grid <= #SMs), so the wait cannot
+    // deadlock, and it is normally already satisfied.
     griddep_wait();  // y / acc / workspace / counters / s_a may belong to the previous kernel
     const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = q * 32 + lane;
-    const bool lead = (warp == kEpiWarp0 && lane == 0);
+    const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
+    const bool lead = et == 0;
+    double* sa_smem = reinterpret_cast<double*>(smem + C::kOffSA);
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
     uint32_t seg = 0;
     while (si.next(tile, kb0, kb1)) {
-      const int j = seg % C::kAccBufs;
-      mbar_wait(&acc_full[j], (seg / C::kAccBufs) & 1);
-      tc_fence_after();
-      if (lead && seg < 4) QQQ_STAMP(36 + 2 * seg);
       const int n_tile = tile / p.tok_tiles;
       const int tok0 = (tile % p.tok_tiles) * NTOK;
+      const int tvalid = (p.M - tok0) < NTOK ? (p.M - tok0) : NTOK;
+      // stage this tile's per-token scales while the MMAs run
+      named_bar_sync(1, kNumEpiWarps * 32);  // previous segment done reading sa_smem
+      for (int t = et; t < tvalid; t += kNumEpiWarps * 32) sa_smem[t] = p.s_a[tok0 + t];
+      named_bar_sync(1, kNumEpiWarps * 32);
       const int n = n_tile * 128 + row;
       const bool n_ok = n < p.N;
-      const int tvalid = (p.M - tok0) < NTOK ? (p.M - tok0) : NTOK;
       const bool whole = (kb0 == 0 && kb1 == p.kb_per_tile);
       const double s_col = (n_ok && p.s_col) ? p.s_col[n] : 0.0;
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
-      const int nchunks = (tvalid + 15) / 16;  // every tile has >= 1 valid token
       int seg_idx = 0, nsegs = 1;
-      int32_t* slot = nullptr;
+      int32_t* slots = nullptr;
       if (!whole) {
         const int64_t u_first = (int64_t)tile * p.kb_per_tile;
         const int b_first = cta_of_unit(u_first, p.units, gridDim.x);
         const int b_last = cta_of_unit(u_first + p.kb_per_tile - 1, p.units, gridDim.x);
         seg_idx = (int)blockIdx.x - b_first;
         nsegs = b_last - b_first + 1;
-        slot = p.ws + ((int64_t)tile * p.max_segs + seg_idx) * NTOK * 128;
+        slots = p.ws + (int64_t)tile * p.max_segs * NTOK * 128;
       }
+      const bool owner = whole || seg_idx == 0;
+      const int j = seg % C::kAccBufs;
+      mbar_wait(&acc_full[j], (seg / C::kAccBufs) & 1);
+      tc_fence_after();
+      if (lead && seg < 4) QQQ_STAMP(36 + 2 * seg);
+      if (!owner) {
+        // ---- contributor: partial -> slot seg_idx, then release the counter
+        int32_t* slot = slots + (int64_t)seg_idx * NTOK * 128 + row;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
+        const int nchunks = (tvalid + 15) / 16;
 #pragma unroll 1
-      for (int c = 0; c < nchunks; ++c) {
-        const int c0 = c * 16;
-        uint32_t r[16];
-        tmem_ld16(taddr + c0, r);
-        tmem_wait_ld();
-        if (c + 1 == nchunks) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&acc_empty[j]);
-        }
-        if (lead && seg == 0 && c < 16) QQQ_STAMP(44 + c);
-        if (whole) {
-          store_outputs(p, r, tok0 + c0, tvalid - c0, n, n_ok, s_col);
-        } else {
+        for (int c = 0; c < nchunks; ++c) {
+          uint32_t r[16];
+          tmem_ld16(taddr + c * 16, r);
+          tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            if (c0 + i < tvalid) __stcg(slot + (c0 + i) * 128 + row, (int32_t)r[i]);
+            if (c * 16 + i < tvalid) __stcg(slot + (c * 16 + i) * 128, (int32_t)r[i]);
         }
-      }
-      if (!whole) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[j]);
         __threadfence();
         named_bar_sync(1, kNumEpiWarps * 32);
-        if (lead) {
-          const int old = atomicAdd(p.counters + tile, 1);
-          *last_flag = (old + 1 == nsegs) ? 1 : 0;
+        if (lead) atomicAdd(p.counters + tile, 1);
+      } else {
+        if (!whole) {
+          // ---- owner of a split tile: wait for the other nsegs-1 partials
+          if (lead) {
+            int32_t* cnt = p.counters + tile;
+            int v;
+            do {
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+            } while (v < nsegs - 1);
+            *cnt = 0;  // re-arm for the next launch (every contributor has arrived)
+          }
+          named_bar_sync(1, kNumEpiWarps * 32);
         }
-        named_bar_sync(1, kNumEpiWarps * 32);
-        const bool last = *last_flag != 0;
-        named_bar_sync(1, kNumEpiWarps * 32);  // last_flag is reused by the next segment
-        if (last) {
-          __threadfence();
-          if (lead) p.counters[tile] = 0;
-          const int32_t* base = p.ws + (int64_t)tile * p.max_segs * NTOK * 128;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
+        const int nchunks = (tvalid + 15) / 16;
 #pragma unroll 1
-          for (int c0 = 0; c0 < tvalid; c0 += 16) {
-            uint32_t r[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) r[i] = 0u;
+        for (int c = 0; c < nchunks; ++c) {
+          const int c0 = c * 16;
+          uint32_t r[16];
+          tmem_ld16(taddr + c0, r);
+          tmem_wait_ld();
+          if (c + 1 == nchunks) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[j]);
+          }
+          if (lead && seg == 0 && c < 16) QQQ_STAMP(44 + c);
+          if (!whole) {
 #pragma unroll 1
-            for (int sg = 0; sg < nsegs; ++sg) {
-              const int32_t* src = base + (int64_t)sg * NTOK * 128 + row;
+            for (int sg = 1; sg < nsegs; ++sg) {
+              const int32_t* src = slots + (int64_t)sg * NTOK * 128 + row;
 #pragma unroll
               for (int i = 0; i < 16; ++i)
                 if (c0 + i < tvalid) r[i] += (uint32_t)__ldcg(src + (c0 + i) * 128);
             }
-            store_outputs(p, r, tok0 + c0, tvalid - c0, n, n_ok, s_col);
           }
+          store_outputs(p, r, sa_smem + c0, tok0 + c0, tvalid - c0, n, n_ok, s_col);
         }
       }
       if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
