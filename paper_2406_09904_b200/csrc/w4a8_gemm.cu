@@ -29,6 +29,7 @@
 //   * Epilogue: f64 (acc * s_a) * s_col then cvt.rn.f16.f64 -> bit-identical
 //     to the reference's f64 epilogue with a single final rounding.
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 
 #include "qqq_common.cuh"
@@ -61,6 +62,7 @@ struct GemmParams {
   int n_tiles, tok_tiles, kb_per_tile, ss_per_tile, ss_bytes, group, max_segs;
   int64_t units;
   int aligned_tiles;        // >0: CTA b owns whole tiles [b*aligned_tiles, ...)
+  int y_tma;                // 1: y written by TMA stores from a shared-memory staging tile
   unsigned long long* dbg;  // optional per-CTA %globaltimer timeline, diagnostics only
 };
 
@@ -81,7 +83,7 @@ struct Cfg {
   static constexpr int kACols = BK / 4;
   static constexpr int kAccBufs = NTOK == 256 ? 1 : 2;
   static constexpr int kAccCols = kAccBufs * NTOK;
-  static constexpr int kRingBudget = kSmemBudget - 4096 - NTOK * 8;
+  static constexpr int kRingBudget = kSmemBudget - 4096 - NTOK * 8 - 2 * 16 * 256;
   static constexpr int kXStagesRaw = (kRingBudget / 4) / kXBytes;  // ~1/4 of the rings to activations
   static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > 8 ? 8 : kXStagesRaw);
   static constexpr int kWStagesRaw = (kRingBudget - kXStages * kXBytes) / kWBytes;
@@ -92,7 +94,8 @@ struct Cfg {
   static constexpr int kOffBar = (kOffW + kWStages * kWBytes + 1023) / 1024 * 1024;
   static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 2 * kABufs + 4;
   static constexpr int kOffSA = kOffBar + (kNumBars * 8 + 16 + 15) / 16 * 16;  // per-token scales of a tile (f64)
-  static constexpr int kSmemBytes = kOffSA + NTOK * 8 + 1024;                // +1024 alignment slack
+  static constexpr int kOffY = (kOffSA + NTOK * 8 + 127) / 128 * 128;          // 2 x [16 tok][128 ch] fp16 staging
+  static constexpr int kSmemBytes = kOffY + 2 * 16 * 256 + 1024;               // +1024 alignment slack
   static_assert(kSmemBytes <= 227 * 1024, "over the per-CTA shared memory limit");
   static constexpr int kTmemNeed = kAccCols + kABufs * kACols;
   static_assert(kTmemNeed <= 512, "TMEM over-subscribed");
@@ -137,22 +140,53 @@ QQQ_DEVICE void tma_load_3d(void* smem_dst, const CUtensorMap* map, int32_t c0, 
       : "memory");
 }
 
+// Exact int32 -> f64 without the (quarter-rate) I2F.F64 unit:
+// 2^52 + 2^31 + a is exactly representable; one DADD removes the bias.
+QQQ_DEVICE double i32_to_f64_exact(int32_t a) {
+  return __hiloint2double(0x43300000, (int)((uint32_t)a ^ 0x80000000u)) - 4503601774854144.0;
+}
+
+// y = f16((acc * s_a[t]) * s_col) for 16 tokens of one channel, branch-free:
+// f64 with one final RN rounding (cvt.rn.f16.f64), as gemm.py:182-184/200-202.
+QQQ_DEVICE void dequant16(const uint32_t (&r)[16], const double* sa, double s_col, uint16_t (&h)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double v = (i32_to_f64_exact((int32_t)r[i]) * sa[i]) * s_col;
+    h[i] = __half_as_ushort(f64_to_f16_rn(v));
+  }
+}
+
 // Dequant epilogue for up to 16 consecutive tokens of one output channel n:
 // y = f16((acc * s_a[t]) * s_col[n]) in f64 with one final RN rounding
 // (gemm.py:182-184 / 200-202); acc written as-is when requested.
+// Direct (per-element) stores: used for the optional int32 acc output and for
+// y when its row pitch does not allow a TMA store.
 QQQ_DEVICE void store_outputs(const GemmParams& p, const uint32_t (&r)[16], const double* sa, int t0, int nvalid,
                               int n, bool n_ok, double s_col) {
   if (!n_ok) return;
+  if (p.acc) {
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    if (i < nvalid) {
-      const int t = t0 + i;
-      const int32_t a = (int32_t)r[i];
-      if (p.acc) p.acc[(int64_t)t * p.ldacc + n] = a;
-      if (p.s_col) p.y[(int64_t)t * p.ldy + n] = f64_to_f16_rn(((double)a * sa[i]) * s_col);
-    }
+    for (int i = 0; i < 16; ++i)
+      if (i < nvalid) p.acc[(int64_t)(t0 + i) * p.ldacc + n] = (int32_t)r[i];
+  }
+  if (p.s_col && !p.y_tma) {
+    uint16_t h[16];
+    dequant16(r, sa, s_col, h);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < nvalid) reinterpret_cast<uint16_t*>(p.y)[(int64_t)(t0 + i) * p.ldy + n] = h[i];
   }
 }
+
+QQQ_DEVICE void tma_store_2d(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+QQQ_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+QQQ_DEVICE void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+QQQ_DEVICE void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Segment iterator: the CTA's contiguous (tile, k-block) unit range split at tile borders.
 struct SegIter {
@@ -197,7 +231,8 @@ QQQ_DEVICE int cta_of_unit(int64_t u, int64_t units, int grid) {
 // ---------------------------------------------------------------------------
 template <int MODE, int NTOK, int BK>
 __global__ void __launch_bounds__(kNumThreads, 1)
-    w4a8_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const GemmParams p) {
+    w4a8_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap y_map,
+                     const GemmParams p) {
   using C = Cfg<MODE, NTOK, BK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -414,6 +449,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
     const bool lead = et == 0;
     double* sa_smem = reinterpret_cast<double*>(smem + C::kOffSA);
+    uint32_t ych = 0;  // y staging chunks issued
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
     uint32_t seg = 0;
@@ -501,11 +537,29 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             }
           }
           store_outputs(p, r, sa_smem + c0, tok0 + c0, tvalid - c0, n, n_ok, s_col);
+          if (p.y_tma) {
+            // y tile chunk -> staging [16 tok][128 ch] fp16 -> one TMA store (OOB rows/cols clipped)
+            uint16_t* stg = reinterpret_cast<uint16_t*>(smem + C::kOffY + (ych & 1) * 4096);
+            if (lead) bulk_wait_read<1>();  // the store that used this buffer two chunks ago has read it
+            named_bar_sync(1, kNumEpiWarps * 32);
+            uint16_t h[16];
+            dequant16(r, sa_smem + c0, s_col, h);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) stg[i * 128 + row] = h[i];
+            fence_proxy_async_smem();
+            named_bar_sync(1, kNumEpiWarps * 32);
+            if (lead) {
+              tma_store_2d(&y_map, stg, n_tile * 128, tok0 + c0);
+              bulk_commit();
+            }
+            ++ych;
+          }
         }
       }
       if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
       ++seg;
     }
+    if (lead) bulk_wait_all();  // y stores complete before the CTA retires
   }
 
   __syncthreads();
@@ -598,7 +652,8 @@ static size_t plan_ws_bytes(const LaunchPlan& lp) {
 }
 
 template <int MODE, int NTOK, int BK>
-static int launch_t(const CUtensorMap& map, const GemmParams& p, int grid, cudaStream_t stream) {
+static int launch_t(const CUtensorMap& map, const CUtensorMap& ymap, const GemmParams& p, int grid,
+                    cudaStream_t stream) {
   using C = Cfg<MODE, NTOK, BK>;
   auto kern = w4a8_gemm_kernel<MODE, NTOK, BK>;
   static bool attr_set = false;  // per instantiation
@@ -617,17 +672,18 @@ static int launch_t(const CUtensorMap& map, const GemmParams& p, int grid, cudaS
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  return cudaLaunchKernelEx(&lc, kern, map, p) == cudaSuccess ? kOk : kErrCuda;
+  return cudaLaunchKernelEx(&lc, kern, map, ymap, p) == cudaSuccess ? kOk : kErrCuda;
 }
 
 template <int MODE>
-static int launch_mode(int ntok, const CUtensorMap& map, const GemmParams& p, int grid, cudaStream_t st) {
+static int launch_mode(int ntok, const CUtensorMap& map, const CUtensorMap& ymap, const GemmParams& p, int grid,
+                       cudaStream_t st) {
   switch (ntok) {
-    case 16: return launch_t<MODE, 16, 256>(map, p, grid, st);
-    case 32: return launch_t<MODE, 32, 256>(map, p, grid, st);
-    case 64: return launch_t<MODE, 64, 256>(map, p, grid, st);
-    case 128: return launch_t<MODE, 128, 128>(map, p, grid, st);
-    case 256: return launch_t<MODE, 256, 128>(map, p, grid, st);
+    case 16: return launch_t<MODE, 16, 256>(map, ymap, p, grid, st);
+    case 32: return launch_t<MODE, 32, 256>(map, ymap, p, grid, st);
+    case 64: return launch_t<MODE, 64, 256>(map, ymap, p, grid, st);
+    case 128: return launch_t<MODE, 128, 128>(map, ymap, p, grid, st);
+    case 256: return launch_t<MODE, 256, 128>(map, ymap, p, grid, st);
     default: return kErrConfig;
   }
 }
@@ -679,7 +735,23 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return kErrCuda;
 
+  // y: fp16 [M, N] (row pitch ldy elements); TMA store box = 128 channels x 16 tokens
+  CUtensorMap ymap;
+  memset(&ymap, 0, sizeof(ymap));
+  int y_tma = 0;
+  if (s_col && y && (ldy * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+    cuuint64_t ydims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+    cuuint64_t ystr[1] = {(cuuint64_t)(ldy * 2)};
+    cuuint32_t ybox[2] = {128u, 16u};
+    cuuint32_t yes[2] = {1u, 1u};
+    if (enc(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, y, ydims, ystr, ybox, yes, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      y_tma = 1;
+  }
+
   GemmParams p{};
+  p.y_tma = y_tma;
   p.w = (const uint8_t*)w_repacked;
   p.s_a = s_a;
   p.s_col = s_col;
@@ -704,9 +776,9 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   p.dbg = cfg ? (unsigned long long*)cfg->dbg : nullptr;
 
   switch (mode) {
-    case kModePC: return launch_mode<kModePC>(lp.ntok, map, p, lp.grid, stream);
-    case kModePG: return launch_mode<kModePG>(lp.ntok, map, p, lp.grid, stream);
-    case kModeI8: return launch_mode<kModeI8>(lp.ntok, map, p, lp.grid, stream);
+    case kModePC: return launch_mode<kModePC>(lp.ntok, map, ymap, p, lp.grid, stream);
+    case kModePG: return launch_mode<kModePG>(lp.ntok, map, ymap, p, lp.grid, stream);
+    case kModeI8: return launch_mode<kModeI8>(lp.ntok, map, ymap, p, lp.grid, stream);
     default: return kErrConfig;
   }
 }
