@@ -28,6 +28,7 @@
 //     epilogue; counters are re-zeroed by that CTA.
 //   * Epilogue: f64 (acc * s_a) * s_col then cvt.rn.f16.f64 -> bit-identical
 //     to the reference's f64 epilogue with a single final rounding.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -605,32 +606,24 @@ struct LaunchPlan {
   int64_t units;
 };
 
-static int pick_ntok(int64_t M) {
-  if (M <= 16) return 16;
-  if (M <= 32) return 32;
-  if (M <= 64) return 64;
-  if (M <= 128) return 128;
-  return 256;
-}
-
-static LaunchPlan make_plan(int64_t M, int64_t N, int64_t K, int force_ntok, int force_grid, int force_split) {
+static LaunchPlan plan_for(int64_t M, int64_t N, int64_t K, int ntok, bool streamk, int force_grid) {
   LaunchPlan lp{};
-  lp.ntok = force_ntok > 0 ? force_ntok : pick_ntok(M);
-  lp.bk = lp.ntok <= 64 ? 256 : 128;
-  lp.tok_tiles = (int)((M + lp.ntok - 1) / lp.ntok);
+  lp.ntok = ntok;
+  lp.bk = ntok <= 64 ? 256 : 128;
+  lp.tok_tiles = (int)((M + ntok - 1) / ntok);
   lp.n_tiles = (int)(round_up(N, kTileN) / kTileN);
   lp.kb_per_tile = (int)(round_up(K, kKPadTo) / lp.bk);
   lp.tiles = lp.n_tiles * lp.tok_tiles;
   lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
   const int sms = num_sms();
-  bool streamk = force_split >= 0 ? force_split == 1 : (lp.ntok <= 64 || lp.tiles < sms / 2);
   lp.max_segs = 1;
   if (streamk) {
     lp.aligned_tiles = 0;
-    lp.grid = (int)(lp.units < sms ? lp.units : sms);
-    if (force_grid > 0) lp.grid = (int)(force_grid < lp.units ? force_grid : lp.units);
-    // most CTAs overlapping one tile
-    const int64_t per = lp.units / lp.grid;  // >= 1
+    // Split tiles are finished by an owner CTA that waits for its contributors,
+    // so every CTA must be co-resident: never more CTAs than SMs (1 CTA/SM).
+    int g = force_grid > 0 ? std::min(force_grid, sms) : sms;
+    lp.grid = (int)(lp.units < g ? lp.units : g);
+    const int64_t per = lp.units / lp.grid;  // >= 1: most CTAs overlapping one tile
     lp.max_segs = (int)((lp.kb_per_tile + per - 1) / per + 1);
     if (lp.max_segs > lp.grid) lp.max_segs = lp.grid;
   } else {
@@ -639,6 +632,47 @@ static LaunchPlan make_plan(int64_t M, int64_t N, int64_t K, int force_ntok, int
     lp.grid = (lp.tiles + per - 1) / per;
   }
   return lp;
+}
+
+// Tile-plan cost model (us), fitted to B200 sweeps of this kernel
+// (scripts/quick_bench.py tile-plan sweeps, profiles/README.md):
+//   T = T0 + units_per_CTA * max(weight bytes / per-CTA HBM share, MMA time,
+//       activation smem traffic) + split-K fix-up + last-tile epilogue.
+static double plan_cost_us(const LaunchPlan& lp) {
+  const double T0 = 1.15, kBsm = 19.6e3, kBtot = 2953e3, kF0 = 4.69, kF1 = 0.046, kE1 = 0.045, kMma = 0.91;
+  const double clk = 1900.0;  // MHz
+  const int64_t ucta = lp.aligned_tiles > 0 ? (int64_t)lp.aligned_tiles * lp.kb_per_tile
+                                            : (lp.units + lp.grid - 1) / lp.grid;
+  const double bw = std::min(kBsm, kBtot / lp.grid);  // bytes/us per CTA
+  const double wkb = lp.bk * 64.0 * (1.0 + 1.0 / 32);
+  const double mma = (lp.bk / 32.0) * (lp.ntok / 2.0) / clk * kMma;
+  const double act = 2.0 * lp.ntok * lp.bk / 128.0 / clk;
+  const double u = std::max(wkb / bw, std::max(mma, act));
+  const double fix = lp.aligned_tiles > 0 ? 0.0 : kF0 + kF1 * lp.ntok;
+  return T0 + ucta * u + fix + kE1 * lp.ntok;
+}
+
+static LaunchPlan make_plan(int64_t M, int64_t N, int64_t K, int force_ntok, int force_grid, int force_split) {
+  if (force_ntok > 0 || force_split >= 0 || force_grid > 0) {
+    const int nt = force_ntok > 0 ? force_ntok : (M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256);
+    const bool sk = force_split >= 0 ? force_split == 1 : nt <= 64;
+    return plan_for(M, N, K, nt, sk, force_grid);
+  }
+  LaunchPlan best{};
+  double best_t = 1e30;
+  for (int nt : {16, 32, 64, 128, 256}) {
+    if (nt > 16 && nt / 2 >= M) break;  // a smaller tile already covers every token
+    for (int sk = 0; sk < 2; ++sk) {
+      const LaunchPlan lp = plan_for(M, N, K, nt, sk == 1, 0);
+      if (lp.tiles > 65536) continue;
+      const double t = plan_cost_us(lp);
+      if (t < best_t) {
+        best_t = t;
+        best = lp;
+      }
+    }
+  }
+  return best;
 }
 
 // Workspace = [kMaxTiles int32 counters (fixed head, zero between launches)]
@@ -694,9 +728,9 @@ using namespace qqq;
 
 extern "C" size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
-  size_t best = 0;  // any plan a caller may force
+  size_t best = 0;  // any plan a caller may force or the cost model may pick
   for (int nt : {16, 32, 64, 128, 256}) {
-    LaunchPlan lp = make_plan(M, N, K, nt, 0, 1);
+    LaunchPlan lp = plan_for(M, N, K, nt, true, 0);
     size_t b = plan_ws_bytes(lp);
     if (b > best) best = b;
   }
