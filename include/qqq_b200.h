@@ -56,6 +56,15 @@ enum { QQQ_MODE_PC = 0, QQQ_MODE_PG = 1, QQQ_MODE_I8 = 2 };
 int qqq_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
                   double* s_a, int32_t* status_dev, qqq_stream_t stream);
 
+/* K-split tensor parallelism (row-parallel linear): the reference scale uses
+ * the FULL row (quantize.py:97-98), so each rank first computes its shard's
+ * row absmax (f64[M]), the ranks all-reduce MAX it, and every rank quantizes
+ * its shard with the global max. Identical codes to the unsplit reference. */
+int qqq_act_absmax(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, double* row_max,
+                   int32_t* status_dev, qqq_stream_t stream);
+int qqq_act_quant_with_max(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, const double* row_max,
+                           int8_t* q, int64_t ldq, double* s_a, int32_t* status_dev, qqq_stream_t stream);
+
 /* ---- offline weight preparation ----------------------------------------- */
 
 /* quant_weight_per_channel (quantize.py:111-123) when group <= 0, else the
@@ -137,6 +146,12 @@ int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a,
                      int64_t group, const double* s_col, int64_t M, int64_t N, int64_t K, void* y, int64_t ldy,
                      int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes, const qqq_gemm_config* cfg,
                      qqq_stream_t stream);
+
+/* The dequant epilogue alone (gemm.py:182-184 / 200-202): y f16 M x N =
+ * f16((acc*s_a)*s_col) in f64; used after an exact int32 all-reduce of K-split
+ * partial accumulators (the GEMM with s_col == NULL returns acc only). */
+int qqq_dequant_epilogue(const int32_t* acc, int64_t M, int64_t N, int64_t ldacc, const double* s_a,
+                         const double* s_col, void* y, int64_t ldy, qqq_stream_t stream);
 
 /* ---- conversion test hooks (the exact device functions the GEMM uses) ---- */
 

@@ -31,6 +31,9 @@ S = c_void_p  # cudaStream_t
 # name -> (restype, argtypes); mirrors include/qqq_b200.h exactly
 SIGNATURES = {
     "qqq_act_quant": (c_int, [P, c_int, I64, I64, I64, P, I64, P, P, S]),
+    "qqq_act_absmax": (c_int, [P, c_int, I64, I64, I64, P, P, S]),
+    "qqq_act_quant_with_max": (c_int, [P, c_int, I64, I64, I64, P, P, I64, P, P, S]),
+    "qqq_dequant_epilogue": (c_int, [P, I64, I64, I64, P, P, P, I64, S]),
     "qqq_quant_weight": (c_int, [P, I64, I64, I64, P, P, P, S]),
     "qqq_requant_scale": (c_int, [P, P, I64, I64, I64, P, S]),
     "qqq_pack_i4": (c_int, [P, I64, I64, P, P, S]),

@@ -71,7 +71,9 @@ QQQ_DEVICE Acc block_max(Acc v, Acc* red) {
 template <typename T, int kThreads>
 __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict__ x, int64_t K, int64_t ldx,
                                                               int8_t* __restrict__ q, int64_t ldq,
-                                                              double* __restrict__ s_out, int32_t* status) {
+                                                              double* __restrict__ s_out, int32_t* status,
+                                                              const double* __restrict__ row_max_in,
+                                                              double* __restrict__ row_max_out) {
   using Acc = typename std::conditional<sizeof(T) == 8, double, float>::type;
   __shared__ Acc red[32];
   // PDL: let the GEMM that consumes q start its prologue / weight prefetch now,
@@ -111,6 +113,11 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
     if (threadIdx.x == 0) atomicOr(status, kStatNonFinite);
   }
   m = block_max<kThreads, Acc>(m, red);
+  if (row_max_out) {  // absmax-only pass (K-split tensor parallelism: all-reduce MAX follows)
+    if (threadIdx.x == 0) row_max_out[row] = (double)m;
+    return;
+  }
+  if (row_max_in) m = (Acc)row_max_in[row];  // the full-row max from the all-reduce (exact: fp16/fp32 values)
   const double s = (m > Acc(0)) ? (double)m / 127.0 : 1.0;
   if (threadIdx.x == 0) s_out[row] = s;
 
@@ -149,9 +156,10 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
 
 using namespace qqq;
 
-extern "C" int qqq_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
-                             double* s_a, int32_t* status_dev, cudaStream_t stream) {
-  if (M < 0 || K <= 0 || ldx < K || ldq < K) return kErrShape;
+static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
+                            double* s_a, int32_t* status_dev, const double* row_max_in, double* row_max_out,
+                            cudaStream_t stream) {
+  if (M < 0 || K <= 0 || ldx < K || (!row_max_out && ldq < K)) return kErrShape;
   if (M == 0) return kOk;
   constexpr int kT = 256;
   cudaLaunchConfig_t lc{};
@@ -166,16 +174,36 @@ extern "C" int qqq_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, i
   cudaError_t e;
   switch (x_dtype) {
     case 0:
-      e = cudaLaunchKernelEx(&lc, act_quant_kernel<__half, kT>, (const __half*)x, K, ldx, q, ldq, s_a, status_dev);
+      e = cudaLaunchKernelEx(&lc, act_quant_kernel<__half, kT>, (const __half*)x, K, ldx, q, ldq, s_a, status_dev,
+                             row_max_in, row_max_out);
       break;
     case 1:
-      e = cudaLaunchKernelEx(&lc, act_quant_kernel<float, kT>, (const float*)x, K, ldx, q, ldq, s_a, status_dev);
+      e = cudaLaunchKernelEx(&lc, act_quant_kernel<float, kT>, (const float*)x, K, ldx, q, ldq, s_a, status_dev,
+                             row_max_in, row_max_out);
       break;
     case 2:
-      e = cudaLaunchKernelEx(&lc, act_quant_kernel<double, kT>, (const double*)x, K, ldx, q, ldq, s_a, status_dev);
+      e = cudaLaunchKernelEx(&lc, act_quant_kernel<double, kT>, (const double*)x, K, ldx, q, ldq, s_a, status_dev,
+                             row_max_in, row_max_out);
       break;
     default:
       return kErrConfig;
   }
   return e == cudaSuccess ? kOk : kErrCuda;
+}
+
+extern "C" int qqq_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
+                             double* s_a, int32_t* status_dev, cudaStream_t stream) {
+  return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, nullptr, nullptr, stream);
+}
+
+extern "C" int qqq_act_absmax(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, double* row_max,
+                              int32_t* status_dev, cudaStream_t stream) {
+  return act_quant_launch(x, x_dtype, M, K, ldx, nullptr, 0, nullptr, status_dev, nullptr, row_max, stream);
+}
+
+extern "C" int qqq_act_quant_with_max(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx,
+                                      const double* row_max, int8_t* q, int64_t ldq, double* s_a, int32_t* status_dev,
+                                      cudaStream_t stream) {
+  if (!row_max) return kErrConfig;
+  return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, row_max, nullptr, stream);
 }

@@ -211,6 +211,17 @@ __global__ void repack8_kernel(const int8_t* __restrict__ w8, const uint8_t* __r
       *reinterpret_cast<const uint4*>(v);
 }
 
+// y = f16((acc * s_a[t]) * s_col[n]) in f64 (gemm.py:182-184 / 200-202): the
+// epilogue applied after an exact int32 all-reduce of K-split partials.
+__global__ void dequant_epilogue_kernel(const int32_t* __restrict__ acc, int64_t M, int64_t N, int64_t ldacc,
+                                        const double* __restrict__ s_a, const double* __restrict__ s_col,
+                                        uint16_t* __restrict__ y, int64_t ldy) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= M * N) return;
+  const int64_t t = idx / N, n = idx % N;
+  y[t * ldy + n] = f64_to_f16_bits(((double)acc[t * ldacc + n] * s_a[t]) * s_col[n]);
+}
+
 // --- exhaustive-test hooks for the device conversion functions --------------
 
 __global__ void fdq_scalar_kernel(const int8_t* q, const uint16_t* s, int8_t* out, int64_t n) {
@@ -363,6 +374,14 @@ extern "C" int qqq_test_pc_convert(const int8_t* q, int8_t* out, int64_t n, cuda
 extern "C" int qqq_test_fast_f16_to_i8(const uint16_t* bits, int8_t* out, int64_t n, cudaStream_t st) {
   if (n <= 0) return kErrShape;
   f16_to_i8_kernel<<<nblk(n, 256), 256, 0, st>>>(bits, out, n);
+  return ok();
+}
+
+extern "C" int qqq_dequant_epilogue(const int32_t* acc, int64_t M, int64_t N, int64_t ldacc, const double* s_a,
+                                    const double* s_col, void* y, int64_t ldy, cudaStream_t st) {
+  if (M < 0 || N <= 0 || ldacc < N || ldy < N) return kErrShape;
+  if (M == 0) return kOk;
+  dequant_epilogue_kernel<<<nblk(M * N, 256), 256, 0, st>>>(acc, M, N, ldacc, s_a, s_col, (uint16_t*)y, ldy);
   return ok();
 }
 
