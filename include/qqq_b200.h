@@ -55,6 +55,12 @@ enum { QQQ_MODE_PC = 0, QQQ_MODE_PG = 1, QQQ_MODE_I8 = 2 };
  * s_a: f64[M]. Bit-exact with the reference (ties included). */
 int qqq_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
                   double* s_a, int32_t* status_dev, qqq_stream_t stream);
+/* Same, also writing rowsum[M] = sum_k q[t, k] (int32), which the per-group
+ * GEMM needs (its weights run as u8 = w8 + 128; acc = acc_u8 - 128*rowsum). */
+int qqq_act_quant_ex(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
+                     double* s_a, int32_t* rowsum, int32_t* status_dev, qqq_stream_t stream);
+/* rowsum of existing int8 codes (activations not produced by qqq_act_quant_ex). */
+int qqq_act_rowsum(const int8_t* q, int64_t M, int64_t K, int64_t ldq, int32_t* rowsum, qqq_stream_t stream);
 
 /* K-split tensor parallelism (row-parallel linear): the reference scale uses
  * the FULL row (quantize.py:97-98), so each rank first computes its shard's
@@ -63,7 +69,8 @@ int qqq_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx,
 int qqq_act_absmax(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, double* row_max,
                    int32_t* status_dev, qqq_stream_t stream);
 int qqq_act_quant_with_max(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, const double* row_max,
-                           int8_t* q, int64_t ldq, double* s_a, int32_t* status_dev, qqq_stream_t stream);
+                           int8_t* q, int64_t ldq, double* s_a, int32_t* rowsum, int32_t* status_dev,
+                           qqq_stream_t stream);
 
 /* ---- offline weight preparation ----------------------------------------- */
 
@@ -128,10 +135,12 @@ int qqq_w4a8_gemm_pc(const int8_t* aq, int64_t ldq, const double* s_a, const voi
                      int64_t ldacc, void* workspace, size_t ws_bytes, qqq_stream_t stream);
 
 /* w4a8_gemm_per_group (gemm.py:188-203): acc = aq . FusedDequantQuant(q, s*),
- * y = f16((acc*s_a)*s_wc); the blob carries s*. group in {32, 64} or k*128. */
-int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked, int64_t group,
-                     const double* s_wc, int64_t M, int64_t N, int64_t K, void* y, int64_t ldy, int32_t* acc_opt,
-                     int64_t ldacc, void* workspace, size_t ws_bytes, qqq_stream_t stream);
+ * y = f16((acc*s_a)*s_wc); the blob carries s*. group in {32, 64} or k*128.
+ * rowsum: sum of each token's int8 codes (qqq_act_quant_ex / qqq_act_rowsum). */
+int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const int32_t* rowsum,
+                     const void* w_repacked, int64_t group, const double* s_wc, int64_t M, int64_t N, int64_t K,
+                     void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
+                     qqq_stream_t stream);
 
 /* Generic form (mode PC/PG/I8) with an optional tile-plan override; I8 with
  * s_col == NULL is gemm_i8_i32 (gemm.py:145-154, acc only). */
@@ -142,10 +151,10 @@ typedef struct qqq_gemm_config {
   void* dbg; /* optional device buffer [grid][64] u64: per-CTA %globaltimer timeline (diagnostics) */
 } qqq_gemm_config;
 
-int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
-                     int64_t group, const double* s_col, int64_t M, int64_t N, int64_t K, void* y, int64_t ldy,
-                     int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes, const qqq_gemm_config* cfg,
-                     qqq_stream_t stream);
+int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const int32_t* rowsum,
+                     const void* w_repacked, int64_t group, const double* s_col, int64_t M, int64_t N, int64_t K,
+                     void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
+                     const qqq_gemm_config* cfg, qqq_stream_t stream);
 
 /* The dequant epilogue alone (gemm.py:182-184 / 200-202): y f16 M x N =
  * f16((acc*s_a)*s_col) in f64; used after an exact int32 all-reduce of K-split

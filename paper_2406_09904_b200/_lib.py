@@ -31,8 +31,10 @@ S = c_void_p  # cudaStream_t
 # name -> (restype, argtypes); mirrors include/qqq_b200.h exactly
 SIGNATURES = {
     "qqq_act_quant": (c_int, [P, c_int, I64, I64, I64, P, I64, P, P, S]),
+    "qqq_act_quant_ex": (c_int, [P, c_int, I64, I64, I64, P, I64, P, P, P, S]),
+    "qqq_act_rowsum": (c_int, [P, I64, I64, I64, P, S]),
     "qqq_act_absmax": (c_int, [P, c_int, I64, I64, I64, P, P, S]),
-    "qqq_act_quant_with_max": (c_int, [P, c_int, I64, I64, I64, P, P, I64, P, P, S]),
+    "qqq_act_quant_with_max": (c_int, [P, c_int, I64, I64, I64, P, P, I64, P, P, P, S]),
     "qqq_dequant_epilogue": (c_int, [P, I64, I64, I64, P, P, P, I64, S]),
     "qqq_quant_weight": (c_int, [P, I64, I64, I64, P, P, P, S]),
     "qqq_requant_scale": (c_int, [P, P, I64, I64, I64, P, S]),
@@ -45,8 +47,8 @@ SIGNATURES = {
     "qqq_repack_weights_i8": (c_int, [P, P, P, I64, I64, I64, P, S]),
     "qqq_gemm_workspace_bytes": (c_size_t, [I64, I64, I64]),
     "qqq_w4a8_gemm_pc": (c_int, [P, I64, P, P, P, I64, I64, I64, P, I64, P, I64, P, c_size_t, S]),
-    "qqq_w4a8_gemm_pg": (c_int, [P, I64, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t, S]),
-    "qqq_w4a8_gemm_ex": (c_int, [c_int, P, I64, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t,
+    "qqq_w4a8_gemm_pg": (c_int, [P, I64, P, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t, S]),
+    "qqq_w4a8_gemm_ex": (c_int, [c_int, P, I64, P, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t,
                                   ctypes.POINTER(GemmConfig), S]),
     "qqq_test_fused_dequant_quant": (c_int, [P, P, P, I64, c_int, S]),
     "qqq_test_pc_convert": (c_int, [P, P, I64, S]),

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
                                                               int8_t* __restrict__ q, int64_t ldq,
                                                               double* __restrict__ s_out, int32_t* status,
                                                               const double* __restrict__ row_max_in,
-                                                              double* __restrict__ row_max_out) {
+                                                              double* __restrict__ row_max_out,
+                                                              int32_t* __restrict__ rowsum_out) {
   using Acc = typename std::conditional<sizeof(T) == 8, double, float>::type;
   __shared__ Acc red[32];
   // PDL: let the GEMM that consumes q start its prologue / weight prefetch now,
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
     }
   };
   const bool qvec_ok = vec_ok && (K % 16 == 0) && ((reinterpret_cast<uintptr_t>(qr) & 15) == 0);
+  int csum = 0;  // sum of this thread's codes (for the u8 x s8 per-group GEMM correction)
   if (qvec_ok) {
     // 16 codes per thread-iteration: 16 * sizeof(T) bytes in, 16 bytes out
     const int64_t n16 = K / 16;
@@ -143,12 +145,46 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
         uint4 pk = __ldg(reinterpret_cast<const uint4*>(xr + i * 16) + h);
         const T* e = reinterpret_cast<const T*>(&pk);
 #pragma unroll
-        for (int j = 0; j < kVec; ++j) out[h * kVec + j] = code(e[j]);
+        for (int j = 0; j < kVec; ++j) {
+          out[h * kVec + j] = code(e[j]);
+          csum += out[h * kVec + j];
+        }
       }
       *reinterpret_cast<uint4*>(qr + i * 16) = *reinterpret_cast<const uint4*>(out);
     }
   } else {
-    for (int64_t i = threadIdx.x; i < K; i += kThreads) qr[i] = code(xr[i]);
+    for (int64_t i = threadIdx.x; i < K; i += kThreads) {
+      const int8_t c = code(xr[i]);
+      qr[i] = c;
+      csum += c;
+    }
+  }
+  if (rowsum_out) {
+    __shared__ int isum[kThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+    if ((threadIdx.x & 31) == 0) isum[threadIdx.x >> 5] = csum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int i = 0; i < kThreads / 32; ++i) t += isum[i];
+      rowsum_out[row] = t;
+    }
+  }
+}
+
+// rowsum of existing int8 codes (activations built outside quant_act_per_token)
+__global__ void rowsum_kernel(const int8_t* __restrict__ q, int64_t K, int64_t ldq, int32_t* __restrict__ out) {
+  const int8_t* qr = q + (int64_t)blockIdx.x * ldq;
+  int s = 0;
+  for (int64_t i = threadIdx.x; i < K; i += blockDim.x) s += qr[i];
+  __shared__ int red[8];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int i = 0; i < (int)(blockDim.x / 32); ++i) t += red[i];
+    out[blockIdx.x] = t;
   }
 }
 
@@ -158,7 +194,7 @@ using namespace qqq;
 
 static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
                             double* s_a, int32_t* status_dev, const double* row_max_in, double* row_max_out,
-                            cudaStream_t stream) {
+                            int32_t* rowsum, cudaStream_t stream) {
   if (M < 0 || K <= 0 || ldx < K || (!row_max_out && ldq < K)) return kErrShape;
   if (M == 0) return kOk;
   constexpr int kT = 256;
@@ -175,15 +211,15 @@ static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, in
   switch (x_dtype) {
     case 0:
       e = cudaLaunchKernelEx(&lc, act_quant_kernel<__half, kT>, (const __half*)x, K, ldx, q, ldq, s_a, status_dev,
-                             row_max_in, row_max_out);
+                             row_max_in, row_max_out, rowsum);
       break;
     case 1:
       e = cudaLaunchKernelEx(&lc, act_quant_kernel<float, kT>, (const float*)x, K, ldx, q, ldq, s_a, status_dev,
-                             row_max_in, row_max_out);
+                             row_max_in, row_max_out, rowsum);
       break;
     case 2:
       e = cudaLaunchKernelEx(&lc, act_quant_kernel<double, kT>, (const double*)x, K, ldx, q, ldq, s_a, status_dev,
-                             row_max_in, row_max_out);
+                             row_max_in, row_max_out, rowsum);
       break;
     default:
       return kErrConfig;
@@ -193,17 +229,30 @@ static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, in
 
 extern "C" int qqq_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
                              double* s_a, int32_t* status_dev, cudaStream_t stream) {
-  return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, nullptr, nullptr, stream);
+  return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, nullptr, nullptr, nullptr, stream);
+}
+
+extern "C" int qqq_act_quant_ex(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q,
+                                int64_t ldq, double* s_a, int32_t* rowsum, int32_t* status_dev, cudaStream_t stream) {
+  return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, nullptr, nullptr, rowsum, stream);
+}
+
+extern "C" int qqq_act_rowsum(const int8_t* q, int64_t M, int64_t K, int64_t ldq, int32_t* rowsum,
+                              cudaStream_t stream) {
+  if (M < 0 || K <= 0 || ldq < K) return kErrShape;
+  if (M == 0) return kOk;
+  rowsum_kernel<<<(unsigned)M, 256, 0, stream>>>(q, K, ldq, rowsum);
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
 }
 
 extern "C" int qqq_act_absmax(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, double* row_max,
                               int32_t* status_dev, cudaStream_t stream) {
-  return act_quant_launch(x, x_dtype, M, K, ldx, nullptr, 0, nullptr, status_dev, nullptr, row_max, stream);
+  return act_quant_launch(x, x_dtype, M, K, ldx, nullptr, 0, nullptr, status_dev, nullptr, row_max, nullptr, stream);
 }
 
 extern "C" int qqq_act_quant_with_max(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx,
-                                      const double* row_max, int8_t* q, int64_t ldq, double* s_a, int32_t* status_dev,
-                                      cudaStream_t stream) {
+                                      const double* row_max, int8_t* q, int64_t ldq, double* s_a, int32_t* rowsum,
+                                      int32_t* status_dev, cudaStream_t stream) {
   if (!row_max) return kErrConfig;
-  return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, row_max, nullptr, stream);
+  return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, row_max, nullptr, rowsum, stream);
 }

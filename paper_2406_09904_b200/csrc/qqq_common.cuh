@@ -205,10 +205,10 @@ QQQ_DEVICE uint64_t make_smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t 
   return d;
 }
 
-// Instruction descriptor for kind::i8: s8 x s8 -> s32, both operands K-major.
-__host__ __device__ constexpr uint32_t make_idesc_i8(uint32_t M, uint32_t N) {
-  return (2u << 4)            // c_format = S32
-         | (1u << 7)          // a_format = signed int8
+// Instruction descriptor for kind::i8: (s8|u8) x s8 -> s32, both operands K-major.
+__host__ __device__ constexpr uint32_t make_idesc_i8(uint32_t M, uint32_t N, bool a_unsigned = false) {
+  return (2u << 4)                      // c_format = S32
+         | ((a_unsigned ? 0u : 1u) << 7)  // a_format: 0 = unsigned, 1 = signed int8
          | (1u << 10)         // b_format = signed int8
          | ((N >> 3) << 17)   // n_dim
          | ((M >> 4) << 24);  // m_dim
@@ -241,17 +241,28 @@ QQQ_DEVICE __half2 u32_as_h2(uint32_t u) { return *reinterpret_cast<__half2*>(&u
 //   FastFP16toINT8: low byte of the fp16 bits, XOR 0x80.
 // kClamp reproduces the reference's out-of-range clamp to [-127, 127]; the
 // repack proves it unnecessary for the weights it accepts on the fast path.
-template <bool kClamp>
-QQQ_DEVICE void pg_convert_word(uint32_t w, __half2 s2, __half2 s2_16, uint32_t& out_lo, uint32_t& out_hi) {
-  const uint32_t kMagic = 0x64006400u;
+// (a & MASK) | c in ONE lop3 (the magic constant is kept in a register so the
+// single-immediate LOP3 encoding can take the mask)
+template <uint32_t MASK>
+QQQ_DEVICE uint32_t and_or(uint32_t a, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "n"(MASK), "r"(c));
+  return d;
+}
+
+// kUnsigned: emit w8 + 128 as an unsigned byte (skip the XOR 0x80); the GEMM
+// then runs a u8 x s8 MMA and subtracts 128 * rowsum(activation codes).
+template <bool kClamp, bool kUnsigned = false>
+QQQ_DEVICE void pg_convert_word(uint32_t w, __half2 s2, __half2 s2_16, uint32_t magic, uint32_t& out_lo,
+                                uint32_t& out_hi) {
   const __half2 k1032 = u32_as_h2(0xE408E408u);  // -1032.0
   const __half2 k1152 = u32_as_h2(0xE480E480u);  // -1152.0
   const __half2 kAdd = u32_as_h2(0x64806480u);   // +1152.0
-  uint32_t a = (w & 0x000F000Fu) | kMagic;
-  uint32_t b = (w & 0x00F000F0u) | kMagic;
+  uint32_t a = and_or<0x000F000Fu>(w, magic);
+  uint32_t b = and_or<0x00F000F0u>(w, magic);
   uint32_t w8 = w >> 8;
-  uint32_t c = (w8 & 0x000F000Fu) | kMagic;
-  uint32_t d = (w8 & 0x00F000F0u) | kMagic;
+  uint32_t c = and_or<0x000F000Fu>(w8, magic);
+  uint32_t d = and_or<0x00F000F0u>(w8, magic);
   __half2 ra = __hfma2(__hadd2(u32_as_h2(a), k1032), s2, kAdd);
   __half2 rb = __hfma2(__hadd2(u32_as_h2(b), k1152), s2_16, kAdd);
   __half2 rc = __hfma2(__hadd2(u32_as_h2(c), k1032), s2, kAdd);
@@ -264,8 +275,12 @@ QQQ_DEVICE void pg_convert_word(uint32_t w, __half2 s2, __half2 s2_16, uint32_t&
     rc = __hmin2(__hmax2(rc, lo), hi);
     rd = __hmin2(__hmax2(rd, lo), hi);
   }
-  out_lo = __byte_perm(h2_as_u32(ra), h2_as_u32(rb), 0x6420) ^ 0x80808080u;
-  out_hi = __byte_perm(h2_as_u32(rc), h2_as_u32(rd), 0x6420) ^ 0x80808080u;
+  out_lo = __byte_perm(h2_as_u32(ra), h2_as_u32(rb), 0x6420);
+  out_hi = __byte_perm(h2_as_u32(rc), h2_as_u32(rd), 0x6420);
+  if (!kUnsigned) {
+    out_lo ^= 0x80808080u;
+    out_hi ^= 0x80808080u;
+  }
 }
 
 // Scalar FusedDequantQuant with the reference's full branch structure

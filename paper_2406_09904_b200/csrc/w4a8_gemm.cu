@@ -52,6 +52,7 @@ constexpr int kDbgSlots = 128;
 struct GemmParams {
   const uint8_t* w;     // repacked weight blob (qqq_layout.cuh)
   const double* s_a;    // [M]
+  const int32_t* rowsum;  // [M] sum of activation codes (per-group u8 x s8 correction)
   const double* s_col;  // [N] s_w_folded (PC) / s_wc (PG); nullptr -> acc only
   __half* y;
   int64_t ldy;
@@ -84,7 +85,7 @@ struct Cfg {
   static constexpr int kACols = BK / 4;
   static constexpr int kAccBufs = NTOK == 256 ? 1 : 2;
   static constexpr int kAccCols = kAccBufs * NTOK;
-  static constexpr int kRingBudget = kSmemBudget - 4096 - NTOK * 8 - 2 * 16 * 256;
+  static constexpr int kRingBudget = kSmemBudget - 4096 - NTOK * 12 - 2 * 16 * 256;
   static constexpr int kXStagesRaw = (kRingBudget / 4) / kXBytes;  // ~1/4 of the rings to activations
   static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > 8 ? 8 : kXStagesRaw);
   static constexpr int kWStagesRaw = (kRingBudget - kXStages * kXBytes) / kWBytes;
@@ -95,14 +96,18 @@ struct Cfg {
   static constexpr int kOffBar = (kOffW + kWStages * kWBytes + 1023) / 1024 * 1024;
   static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 2 * kABufs + 4;
   static constexpr int kOffSA = kOffBar + (kNumBars * 8 + 16 + 15) / 16 * 16;  // per-token scales of a tile (f64)
-  static constexpr int kOffY = (kOffSA + NTOK * 8 + 127) / 128 * 128;          // 2 x [16 tok][128 ch] fp16 staging
+  static constexpr int kOffRS = kOffSA + NTOK * 8;                             // per-token code sums (int32)
+  static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;          // 2 x [16 tok][128 ch] fp16 staging
   static constexpr int kSmemBytes = kOffY + 2 * 16 * 256 + 1024;               // +1024 alignment slack
   static_assert(kSmemBytes <= 227 * 1024, "over the per-CTA shared memory limit");
   static constexpr int kTmemNeed = kAccCols + kABufs * kACols;
   static_assert(kTmemNeed <= 512, "TMEM over-subscribed");
   static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
                                         : kTmemNeed <= 256 ? 256 : 512;
-  static constexpr uint32_t kIdesc = make_idesc_i8(128, NTOK);
+  // per-group: the converter emits w8 + 128 (no XOR); the MMA runs u8 x s8 and
+  // the epilogue subtracts 128 * rowsum(a) — exact in int32 (K <= 65536)
+  static constexpr bool kU8 = MODE == kModePG;
+  static constexpr uint32_t kIdesc = make_idesc_i8(128, NTOK, kU8);
   static_assert(NTOK % 16 == 0 && NTOK >= 16 && NTOK <= 256, "invalid UMMA N");
   static_assert(BK % 128 == 0, "BK must be a multiple of the 128-byte swizzle atom");
 };
@@ -379,6 +384,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int q = warp & 3, h = (warp >> 2) & 1;
       const int row = q * 32 + lane;
       const int geff = p.group < 128 ? p.group : 128;
+      uint32_t magic;
+      asm("mov.b32 %0, 0x64006400;" : "=r"(magic));  // a register operand for the fused and-or lop3
       const uint32_t a_lane = tmem_base + ((uint32_t)(q * 32) << 16) + C::kAccCols;
       SegIter si = make_iter(p);
       int tile, kb0, kb1;
@@ -411,10 +418,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             } else {
               const __half2 s2 = __halves2half2(s1[i], s1[i]);
               const __half2 s16 = __hmul2(s2, u32_as_h2(0x2C002C00u));  // * 1/16
-              pg_convert_word<false>(v[i].x, s2, s16, o[i][0], o[i][1]);
-              pg_convert_word<false>(v[i].y, s2, s16, o[i][2], o[i][3]);
-              pg_convert_word<false>(v[i].z, s2, s16, o[i][4], o[i][5]);
-              pg_convert_word<false>(v[i].w, s2, s16, o[i][6], o[i][7]);
+              pg_convert_word<false, true>(v[i].x, s2, s16, magic, o[i][0], o[i][1]);
+              pg_convert_word<false, true>(v[i].y, s2, s16, magic, o[i][2], o[i][3]);
+              pg_convert_word<false, true>(v[i].z, s2, s16, magic, o[i][4], o[i][5]);
+              pg_convert_word<false, true>(v[i].w, s2, s16, magic, o[i][6], o[i][7]);
             }
           }
           // the packed stage is consumed (values are in registers): release it now
@@ -450,6 +457,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
     const bool lead = et == 0;
     double* sa_smem = reinterpret_cast<double*>(smem + C::kOffSA);
+    int32_t* rs_smem = reinterpret_cast<int32_t*>(smem + C::kOffRS);
     uint32_t ych = 0;  // y staging chunks issued
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
@@ -460,7 +468,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int tvalid = (p.M - tok0) < NTOK ? (p.M - tok0) : NTOK;
       // stage this tile's per-token scales while the MMAs run
       named_bar_sync(1, kNumEpiWarps * 32);  // previous segment done reading sa_smem
-      for (int t = et; t < tvalid; t += kNumEpiWarps * 32) sa_smem[t] = p.s_a[tok0 + t];
+      for (int t = et; t < tvalid; t += kNumEpiWarps * 32) {
+        sa_smem[t] = p.s_a[tok0 + t];
+        if constexpr (C::kU8) rs_smem[t] = 128 * p.rowsum[tok0 + t];
+      }
       named_bar_sync(1, kNumEpiWarps * 32);
       const int n = n_tile * 128 + row;
       const bool n_ok = n < p.N;
@@ -536,6 +547,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               for (int i = 0; i < 16; ++i)
                 if (c0 + i < tvalid) r[i] += (uint32_t)__ldcg(src + (c0 + i) * 128);
             }
+          }
+          if constexpr (C::kU8) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) r[i] -= (uint32_t)rs_smem[c0 + i];  // u8 weights carried +128
           }
           store_outputs(p, r, sa_smem + c0, tok0 + c0, tvalid - c0, n, n_ok, s_col);
           if (p.y_tma) {
@@ -738,14 +753,15 @@ extern "C" size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
 }
 
 // Generic entry: mode 0 = per-channel (PC), 1 = per-group (PG), 2 = pre-converted int8 (I8).
-extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
-                                int64_t group, const double* s_col, int64_t M, int64_t N, int64_t K, void* y,
-                                int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
-                                const qqq_gemm_config* cfg, cudaStream_t stream) {
+extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const int32_t* rowsum,
+                                const void* w_repacked, int64_t group, const double* s_col, int64_t M, int64_t N,
+                                int64_t K, void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace,
+                                size_t ws_bytes, const qqq_gemm_config* cfg, cudaStream_t stream) {
   if (M < 0 || N <= 0 || K <= 0) return kErrShape;
   if (K > (1 << 16)) return kErrShape;  // gemm.py:49,151
   if (M == 0) return kOk;
   if (mode == kModePG && !pg_group_ok(group)) return kErrUnsupported;
+  if (mode == kModePG && !rowsum) return kErrConfig;
   // 3-D activation view {128, M, ceil(K/128)}: rows must hold round_up(K, 128) bytes
   if ((ldq % 16) != 0 || ldq < round_up(K, 128) || (reinterpret_cast<uintptr_t>(aq) & 15) != 0)
     return kErrUnsupported;
@@ -788,6 +804,7 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   p.y_tma = y_tma;
   p.w = (const uint8_t*)w_repacked;
   p.s_a = s_a;
+  p.rowsum = rowsum;
   p.s_col = s_col;
   p.y = (__half*)y;
   p.ldy = ldy;
@@ -820,14 +837,14 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
 extern "C" int qqq_w4a8_gemm_pc(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
                                 const double* s_w_folded, int64_t M, int64_t N, int64_t K, void* y, int64_t ldy,
                                 int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes, cudaStream_t stream) {
-  return qqq_w4a8_gemm_ex(kModePC, aq, ldq, s_a, w_repacked, 0, s_w_folded, M, N, K, y, ldy, acc_opt, ldacc,
+  return qqq_w4a8_gemm_ex(kModePC, aq, ldq, s_a, nullptr, w_repacked, 0, s_w_folded, M, N, K, y, ldy, acc_opt, ldacc,
                           workspace, ws_bytes, nullptr, stream);
 }
 
-extern "C" int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
-                                int64_t group, const double* s_wc, int64_t M, int64_t N, int64_t K, void* y,
-                                int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
-                                cudaStream_t stream) {
-  return qqq_w4a8_gemm_ex(kModePG, aq, ldq, s_a, w_repacked, group, s_wc, M, N, K, y, ldy, acc_opt, ldacc,
+extern "C" int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const int32_t* rowsum,
+                                const void* w_repacked, int64_t group, const double* s_wc, int64_t M, int64_t N,
+                                int64_t K, void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace,
+                                size_t ws_bytes, cudaStream_t stream) {
+  return qqq_w4a8_gemm_ex(kModePG, aq, ldq, s_a, rowsum, w_repacked, group, s_wc, M, N, K, y, ldy, acc_opt, ldacc,
                           workspace, ws_bytes, nullptr, stream);
 }

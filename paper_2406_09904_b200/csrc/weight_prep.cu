@@ -239,7 +239,7 @@ __global__ void fdq_word_kernel(const int8_t* q, const uint16_t* s, int8_t* out,
   const __half2 s2 = __halves2half2(s1, s1);
   const __half2 s16 = __hmul2(s2, u32_as_h2(0x2C002C00u));
   uint32_t lo, hi;
-  pg_convert_word<false>(w, s2, s16, lo, hi);
+  pg_convert_word<false>(w, s2, s16, 0x64006400u, lo, hi);
   reinterpret_cast<uint32_t*>(out)[2 * i] = lo;
   reinterpret_cast<uint32_t*>(out)[2 * i + 1] = hi;
 }

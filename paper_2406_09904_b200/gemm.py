@@ -28,6 +28,7 @@ from .quantize import (
     QuantizedWeights,
     as_cuda,
     raise_if_bad,
+    rowsum_of,
 )
 
 __all__ = [
@@ -221,7 +222,8 @@ def run_gemm(aq: QuantizedActivations, prep: PreparedWeights, n: int, with_acc: 
         c = _lib.GemmConfig(int(cfg.get("ntok", 0)), int(cfg.get("grid", 0)), int(cfg.get("split", -1)),
                             None if dbg is None else dbg.data_ptr())
     ldq = q.stride(0) if m > 1 else (k + 127) // 128 * 128
-    rc = lib.qqq_w4a8_gemm_ex(prep.mode, _lib.ptr(q), ldq, _lib.ptr(s_a), _lib.ptr(prep.w),
+    rs = rowsum_of(aq) if prep.mode == _lib.MODE_PG else None
+    rc = lib.qqq_w4a8_gemm_ex(prep.mode, _lib.ptr(q), ldq, _lib.ptr(s_a), _lib.ptr(rs), _lib.ptr(prep.w),
                               prep.group, _lib.ptr(prep.s_col), m, n, k, _lib.ptr(y), y.stride(0),
                               _lib.ptr(acc), n, _lib.ptr(ws), ws.numel(),
                               None if c is None else c, _lib.stream_of(dev))
@@ -285,7 +287,7 @@ def gemm_i8_i32(aq, w8) -> torch.Tensor:
         return acc
     ws = workspace(dev, lib.qqq_gemm_workspace_bytes(m, n, k))
     ldq = q.stride(0) if m > 1 else (k + 127) // 128 * 128
-    _lib.check(lib.qqq_w4a8_gemm_ex(_lib.MODE_I8, _lib.ptr(q), ldq, _lib.ptr(aqq.s_a), _lib.ptr(prep.w),
+    _lib.check(lib.qqq_w4a8_gemm_ex(_lib.MODE_I8, _lib.ptr(q), ldq, _lib.ptr(aqq.s_a), None, _lib.ptr(prep.w),
                                     0, None, m, n, k, None, n, _lib.ptr(acc), n, _lib.ptr(ws), ws.numel(), None,
                                     _lib.stream_of(dev)), "gemm_i8_i32")
     return acc

@@ -133,18 +133,49 @@ def quant_act_per_token(x, check: bool = True) -> QuantizedActivations:
     kp = (k + 127) // 128 * 128  # row pitch = whole 128-byte atoms for the GEMM's TMA; view is M x K
     qbuf = torch.empty((m, kp), dtype=torch.int8, device=dev)
     s_a = torch.empty((m,), dtype=torch.float64, device=dev)
+    rowsum = torch.empty((m,), dtype=torch.int32, device=dev)
     status = _status(dev)
     if m > 0 and k > 0:
         dt = {torch.float16: 0, torch.float32: 1, torch.float64: 2}[xt.dtype]
-        _lib.check(lib.qqq_act_quant(_lib.ptr(xt), dt, m, k, ldx, _lib.ptr(qbuf), kp, _lib.ptr(s_a),
-                                     _lib.ptr(status), _lib.stream_of(dev)), "quant_act_per_token")
+        _lib.check(lib.qqq_act_quant_ex(_lib.ptr(xt), dt, m, k, ldx, _lib.ptr(qbuf), kp, _lib.ptr(s_a),
+                                        _lib.ptr(rowsum), _lib.ptr(status), _lib.stream_of(dev)),
+                   "quant_act_per_token")
     elif k == 0:
         raise ShapeError("activations must have K >= 1")
     out = QuantizedActivations(q=qbuf[:, :k], s_a=s_a)
+    attach_rowsum(out, rowsum)
     if check:
         raise_if_bad(status, "activations")
     else:
         out._status = status  # type: ignore[attr-defined]
+    return out
+
+
+def _q_key(q: torch.Tensor):
+    return (q.data_ptr(), q._version, tuple(q.shape))
+
+
+def attach_rowsum(aq: QuantizedActivations, rowsum: torch.Tensor) -> None:
+    """Cache sum_k q[t, k] on the activations (valid while aq.q is unmodified)."""
+    aq._rowsum = (_q_key(aq.q), rowsum)  # type: ignore[attr-defined]
+
+
+def rowsum_of(aq: QuantizedActivations) -> torch.Tensor:
+    """int32 per-token code sums, cached or recomputed on the GPU if aq.q changed."""
+    hit = getattr(aq, "_rowsum", None)
+    q = as_cuda(aq.q, torch.int8)
+    if hit is not None and hit[0] == _q_key(aq.q):
+        return hit[1]
+    m, k = q.shape
+    out = torch.empty((m,), dtype=torch.int32, device=q.device)
+    if m:
+        if q.stride(1) != 1:
+            q = q.contiguous()
+        lib = _lib.lib_for_device(q.device)
+        _lib.check(lib.qqq_act_rowsum(_lib.ptr(q), m, k, q.stride(0) if m > 1 else k, _lib.ptr(out),
+                                      _lib.stream_of(q.device)), "act_rowsum")
+    if isinstance(aq.q, torch.Tensor) and aq.q.is_cuda:
+        attach_rowsum(aq, out)
     return out
 
 

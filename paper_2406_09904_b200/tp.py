@@ -30,7 +30,7 @@ import torch.distributed as dist
 from . import _lib
 from .errors import ConfigError, ShapeError
 from .gemm import FusedScales, prepare, run_gemm
-from .quantize import PER_CHANNEL, PER_GROUP, QuantizedActivations, QuantizedWeights, as_cuda
+from .quantize import PER_CHANNEL, PER_GROUP, QuantizedActivations, QuantizedWeights, as_cuda, attach_rowsum
 
 __all__ = ["shard_nsplit", "shard_ksplit", "TPOps", "ColumnParallelW4A8", "RowParallelW4A8"]
 
@@ -105,12 +105,15 @@ class TPOps:
         kp = (k + 127) // 128 * 128
         q = torch.empty((m, kp), dtype=torch.int8, device=x.device)
         s_a = torch.empty(m, dtype=torch.float64, device=x.device)
+        rowsum = torch.empty(m, dtype=torch.int32, device=x.device)
         status = torch.zeros(1, dtype=torch.int32, device=x.device)
         dt = {torch.float16: 0, torch.float32: 1, torch.float64: 2}[x.dtype]
         _lib.check(lib.qqq_act_quant_with_max(_lib.ptr(x), dt, m, k, k, _lib.ptr(row_max.contiguous()), _lib.ptr(q),
-                                              kp, _lib.ptr(s_a), _lib.ptr(status), _lib.stream_of(x.device)),
-                   "act_quant_with_max")
-        return QuantizedActivations(q=q[:, :k], s_a=s_a)
+                                              kp, _lib.ptr(s_a), _lib.ptr(rowsum), _lib.ptr(status),
+                                              _lib.stream_of(x.device)), "act_quant_with_max")
+        aq = QuantizedActivations(q=q[:, :k], s_a=s_a)
+        attach_rowsum(aq, rowsum)
+        return aq
 
     def gemm(self, aq, qw, fused) -> torch.Tensor:
         return run_gemm(aq, prepare(qw, fused), qw.cols, with_acc=False).y
