@@ -122,8 +122,14 @@ __global__ void repack4_kernel(const uint8_t* __restrict__ packed, int64_t K, in
   const int64_t slab = blockIdx.y;
   if (n >= N_pad) return;
   int u[32];
+  // Padding k >= K: per-channel/I8 use the zero code (signed MMA). Per-group runs
+  // the MMA on u8 = w8 + 128, so padding must be u8 0: code q = -8 with the
+  // padding scale s* = 16 gives RN(-8*16 + 1152) = 1024 -> byte 0 exactly.
 #pragma unroll
-  for (int e = 0; e < 32; ++e) u[e] = ref_nibble(packed, K, N, slab * 32 + e, n);
+  for (int e = 0; e < 32; ++e) {
+    const int64_t k = slab * 32 + e;
+    u[e] = (mode == kModePG && k >= K) ? 0 : ref_nibble(packed, K, N, k, n);
+  }
   uint32_t wd[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -160,7 +166,7 @@ __global__ void repack_scales_kernel(const uint16_t* __restrict__ s_star, const 
   if (n >= N_pad) return;
   const int64_t geff = group < 128 ? group : 128;
   const int64_t k0 = ss * 128 + gl * geff;  // first k of this chunk
-  uint16_t h = 0;
+  uint16_t h = k0 >= K ? (uint16_t)0x4C00 : (uint16_t)0;  // K padding: s* = 16 (see repack4_kernel)
   if (k0 < K && n < N) {
     h = s_star[(k0 / group) * N + n];
     int qmin = 7, qmax = -8;
