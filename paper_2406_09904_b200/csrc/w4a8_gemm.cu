@@ -58,7 +58,7 @@ struct GemmParams {
   int64_t ldy;
   int32_t* acc;  // optional
   int64_t ldacc;
-  int32_t* ws;        // split-K partials [tiles][max_segs][NTOK][128] int32 (no init needed)
+  int32_t* ws;        // split-K accumulation slots [tiles][NTOK][128] int32, zero on entry and exit
   int32_t* counters;  // [tiles] arrival counters at the fixed head of the workspace; zero on entry and exit
   int M, N, K;
   int n_tiles, tok_tiles, kb_per_tile, ss_per_tile, ss_bytes, group, max_segs;
@@ -85,8 +85,11 @@ struct Cfg {
   static constexpr int kACols = BK / 4;
   static constexpr int kAccBufs = NTOK == 256 ? 1 : 2;
   static constexpr int kAccCols = kAccBufs * NTOK;
-  static constexpr int kRingBudget = kSmemBudget - 4096 - NTOK * 12 - 2 * 16 * 256;
-  static constexpr int kXStagesRaw = (kRingBudget / 4) / kXBytes;  // ~1/4 of the rings to activations
+  static constexpr int kRingBudget = kSmemBudget - 4096 - NTOK * 12 - 2 * 16 * 256 - 2 * 8192;
+  // activations get what is left after >= 4 weight stages (capped at 8): small
+  // for decode tiles, and deep enough at large NTOK that the L2->smem latency of
+  // a 32 KiB activation tile is hidden
+  static constexpr int kXStagesRaw = (kRingBudget - 4 * kWBytes) / kXBytes;
   static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > 8 ? 8 : kXStagesRaw);
   static constexpr int kWStagesRaw = (kRingBudget - kXStages * kXBytes) / kWBytes;
   static constexpr int kWStages = kWStagesRaw > 12 ? 12 : kWStagesRaw;
@@ -94,11 +97,12 @@ struct Cfg {
   static constexpr int kOffX = 0;  // 1024-aligned: NTOK*BK is a multiple of 2048
   static constexpr int kOffW = kOffX + kXStages * kXBytes;
   static constexpr int kOffBar = (kOffW + kWStages * kWBytes + 1023) / 1024 * 1024;
-  static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 2 * kABufs + 4;
+  static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 2 * kABufs + 4 + 2;
   static constexpr int kOffSA = kOffBar + (kNumBars * 8 + 16 + 15) / 16 * 16;  // per-token scales of a tile (f64)
   static constexpr int kOffRS = kOffSA + NTOK * 8;                             // per-token code sums (int32)
   static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;          // 2 x [16 tok][128 ch] fp16 staging
-  static constexpr int kSmemBytes = kOffY + 2 * 16 * 256 + 1024;               // +1024 alignment slack
+  static constexpr int kOffPart = kOffY + 2 * 16 * 256;                        // 2 x 8 KiB split-K partial chunks
+  static constexpr int kSmemBytes = kOffPart + 2 * 8192 + 1024;                 // +1024 alignment slack
   static_assert(kSmemBytes <= 227 * 1024, "over the per-CTA shared memory limit");
   static constexpr int kTmemNeed = kAccCols + kABufs * kACols;
   static_assert(kTmemNeed <= 512, "TMEM over-subscribed");
@@ -135,6 +139,10 @@ QQQ_DEVICE __half f64_to_f16_rn(double v) {
   unsigned short h;
   asm("cvt.rn.f16.f64 %0, %1;" : "=h"(h) : "d"(v));
   return __ushort_as_half(h);
+}
+
+QQQ_DEVICE void red_add_s32(int32_t* p, int32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 QQQ_DEVICE void tma_load_3d(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
@@ -251,6 +259,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* a_empty = a_full + C::kABufs;
   uint64_t* acc_full = a_empty + C::kABufs;
   uint64_t* acc_empty = acc_full + 2;
+  uint64_t* part_full = acc_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = threadIdx.x >> 5;
@@ -275,6 +284,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       mbar_init(&acc_full[j], 1);
       mbar_init(&acc_empty[j], kNumEpiWarps);
     }
+    mbar_init(&part_full[0], 1);
+    mbar_init(&part_full[1], 1);
     mbar_fence_init();
   }
   if (warp == kActProducerWarp && lane == 0) tma_prefetch_desc(&act_map);
@@ -458,7 +469,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const bool lead = et == 0;
     double* sa_smem = reinterpret_cast<double*>(smem + C::kOffSA);
     int32_t* rs_smem = reinterpret_cast<int32_t*>(smem + C::kOffRS);
-    uint32_t ych = 0;  // y staging chunks issued
+    uint32_t ych = 0;     // y staging chunks issued
+    uint32_t pchunk = 0;  // partial-sum chunks consumed (parity of the part_full ring)
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
     uint32_t seg = 0;
@@ -485,7 +497,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         const int b_last = cta_of_unit(u_first + p.kb_per_tile - 1, p.units, gridDim.x);
         seg_idx = (int)blockIdx.x - b_first;
         nsegs = b_last - b_first + 1;
-        slots = p.ws + (int64_t)tile * p.max_segs * NTOK * 128;
+        slots = p.ws + (int64_t)tile * NTOK * 128;  // one zero-initialised accumulation slot per tile
       }
       const bool owner = whole || seg_idx == 0;
       const int j = seg % C::kAccBufs;
@@ -493,8 +505,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       tc_fence_after();
       if (lead && seg < 4) QQQ_STAMP(36 + 2 * seg);
       if (!owner) {
-        // ---- contributor: partial -> slot seg_idx, then release the counter
-        int32_t* slot = slots + (int64_t)seg_idx * NTOK * 128 + row;
+        // ---- contributor: red.add the partial into the tile's slot, release the counter
+        int32_t* slot = slots + row;
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
         const int nchunks = (tvalid + 15) / 16;
 #pragma unroll 1
@@ -504,7 +516,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            if (c * 16 + i < tvalid) __stcg(slot + (c * 16 + i) * 128, (int32_t)r[i]);
+            if (c * 16 + i < tvalid) red_add_s32(slot + (c * 16 + i) * 128, (int32_t)r[i]);
         }
         tc_fence_before();
         __syncwarp();
@@ -527,6 +539,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
         const int nchunks = (tvalid + 15) / 16;
+        // reduced partial chunks [16 tok][128 rows] int32 (8 KiB, contiguous in the
+        // slot) are bulk-copied into a 2-deep smem ring, one chunk ahead
+        auto part_issue = [&](int c) {
+          const uint32_t pc = pchunk + c;
+          uint8_t* dst = smem + C::kOffPart + (pc & 1) * 8192;
+          mbar_arrive_expect_tx(&part_full[pc & 1], 8192);
+          bulk_g2s(dst, slots + (int64_t)c * 16 * 128, 8192, &part_full[pc & 1]);
+        };
+        if (!whole && lead) {
+          part_issue(0);
+          if (nchunks > 1) part_issue(1);
+        }
 #pragma unroll 1
         for (int c = 0; c < nchunks; ++c) {
           const int c0 = c * 16;
@@ -540,13 +564,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
           if (lead && seg == 0 && c < 16) QQQ_STAMP(44 + c);
           if (!whole) {
-#pragma unroll 1
-            for (int sg = 1; sg < nsegs; ++sg) {
-              const int32_t* src = slots + (int64_t)sg * NTOK * 128 + row;
+            const uint32_t pc = pchunk + c;
+            mbar_wait(&part_full[pc & 1], (pc >> 1) & 1);
+            const int32_t* part = reinterpret_cast<const int32_t*>(smem + C::kOffPart + (pc & 1) * 8192);
 #pragma unroll
-              for (int i = 0; i < 16; ++i)
-                if (c0 + i < tvalid) r[i] += (uint32_t)__ldcg(src + (c0 + i) * 128);
-            }
+            for (int i = 0; i < 16; ++i) r[i] += (uint32_t)part[i * 128 + row];
+            // return the slot to zero for the next launch (entries past tvalid were never touched)
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < tvalid) __stcg(slots + (c0 + i) * 128 + row, 0);
+            named_bar_sync(1, kNumEpiWarps * 32);  // every thread has read this buffer
+            if (lead && c + 2 < nchunks) part_issue(c + 2);
           }
           if constexpr (C::kU8) {
 #pragma unroll
@@ -572,6 +600,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
         }
       }
+      if (owner && !whole) pchunk += (tvalid + 15) / 16;
       if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
       ++seg;
     }
@@ -697,7 +726,7 @@ constexpr size_t kCounterBytes = (size_t)kMaxTiles * 4;
 
 static size_t plan_ws_bytes(const LaunchPlan& lp) {
   if (lp.aligned_tiles > 0) return kCounterBytes;
-  return kCounterBytes + (size_t)lp.tiles * lp.max_segs * lp.ntok * 128 * 4;
+  return kCounterBytes + (size_t)lp.tiles * lp.ntok * 128 * 4;
 }
 
 template <int MODE, int NTOK, int BK>
