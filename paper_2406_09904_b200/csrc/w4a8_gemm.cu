@@ -40,11 +40,11 @@ namespace qqq {
 
 constexpr int kNumConvWarps = 8;
 constexpr int kConvWarp0 = 0;
-constexpr int kEpiWarp0 = kNumConvWarps, kNumEpiWarps = 4;
-constexpr int kAllocWarp = kEpiWarp0 + 4;
-constexpr int kActProducerWarp = kEpiWarp0 + 5;
-constexpr int kWProducerWarp = kEpiWarp0 + 6;
-constexpr int kMmaWarp = kEpiWarp0 + 7;
+constexpr int kEpiWarp0 = kNumConvWarps, kNumEpiWarps = 8;  // two halves of 4 (one per TMEM lane quadrant)
+constexpr int kAllocWarp = kEpiWarp0 + kNumEpiWarps;
+constexpr int kActProducerWarp = kAllocWarp + 1;
+constexpr int kWProducerWarp = kAllocWarp + 2;
+constexpr int kMmaWarp = kAllocWarp + 3;
 constexpr int kNumThreads = (kMmaWarp + 1) * 32;
 constexpr int kSmemBudget = 225 * 1024;
 constexpr int kDbgSlots = 128;
@@ -85,7 +85,7 @@ struct Cfg {
   static constexpr int kACols = BK / 4;
   static constexpr int kAccBufs = NTOK == 256 ? 1 : 2;
   static constexpr int kAccCols = kAccBufs * NTOK;
-  static constexpr int kRingBudget = kSmemBudget - 4096 - NTOK * 12 - 2 * 16 * 256 - 2 * 8192;
+  static constexpr int kRingBudget = kSmemBudget - 4096 - NTOK * 12 - 2 * 2 * 16 * 256 - 2 * 2 * 8192;
   // activations get what is left after >= 4 weight stages (capped at 8): small
   // for decode tiles, and deep enough at large NTOK that the L2->smem latency of
   // a 32 KiB activation tile is hidden
@@ -97,12 +97,12 @@ struct Cfg {
   static constexpr int kOffX = 0;  // 1024-aligned: NTOK*BK is a multiple of 2048
   static constexpr int kOffW = kOffX + kXStages * kXBytes;
   static constexpr int kOffBar = (kOffW + kWStages * kWBytes + 1023) / 1024 * 1024;
-  static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 2 * kABufs + 4 + 2;
+  static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 2 * kABufs + 4 + 4;
   static constexpr int kOffSA = kOffBar + (kNumBars * 8 + 16 + 15) / 16 * 16;  // per-token scales of a tile (f64)
   static constexpr int kOffRS = kOffSA + NTOK * 8;                             // per-token code sums (int32)
-  static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;          // 2 x [16 tok][128 ch] fp16 staging
-  static constexpr int kOffPart = kOffY + 2 * 16 * 256;                        // 2 x 8 KiB split-K partial chunks
-  static constexpr int kSmemBytes = kOffPart + 2 * 8192 + 1024;                 // +1024 alignment slack
+  static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;  // per epilogue half: 2 x [16 tok][128 ch] fp16
+  static constexpr int kOffPart = kOffY + 2 * 2 * 16 * 256;            // per half: 2 x 8 KiB split-K partial chunks
+  static constexpr int kSmemBytes = kOffPart + 2 * 2 * 8192 + 1024;     // +1024 alignment slack
   static_assert(kSmemBytes <= 227 * 1024, "over the per-CTA shared memory limit");
   static constexpr int kTmemNeed = kAccCols + kABufs * kACols;
   static_assert(kTmemNeed <= 512, "TMEM over-subscribed");
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* a_empty = a_full + C::kABufs;
   uint64_t* acc_full = a_empty + C::kABufs;
   uint64_t* acc_empty = acc_full + 2;
-  uint64_t* part_full = acc_empty + 2;
+  uint64_t* part_full = acc_empty + 2;  // [half][2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = threadIdx.x >> 5;
@@ -284,8 +284,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       mbar_init(&acc_full[j], 1);
       mbar_init(&acc_empty[j], kNumEpiWarps);
     }
-    mbar_init(&part_full[0], 1);
-    mbar_init(&part_full[1], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&part_full[i], 1);
     mbar_fence_init();
   }
   if (warp == kActProducerWarp && lane == 0) tma_prefetch_desc(&act_map);
@@ -463,14 +462,23 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // CTAs of the grid are co-resident (grid <= #SMs), so the wait cannot
     // deadlock, and it is normally already satisfied.
     griddep_wait();  // y / acc / workspace / counters / s_a may belong to the previous kernel
+    // two halves of 4 warps (each covering all 128 TMEM lanes) take alternate
+    // 16-token chunks: half the per-thread work, same TMEM/partial/y protocol
+    const int eh = (warp - kEpiWarp0) >> 2;
     const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = q * 32 + lane;
-    const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
-    const bool lead = et == 0;
+    const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..255
+    const bool lead = et == 0;                    // segment-level lead (counters)
+    const bool hlead = (et & 127) == 0;           // half lead (TMA stores, partial prefetch)
+    const int kBarAll = 1, kBarHalf = 2 + eh;
+    constexpr int kAll = kNumEpiWarps * 32, kHalf = kAll / 2;
     double* sa_smem = reinterpret_cast<double*>(smem + C::kOffSA);
     int32_t* rs_smem = reinterpret_cast<int32_t*>(smem + C::kOffRS);
-    uint32_t ych = 0;     // y staging chunks issued
-    uint32_t pchunk = 0;  // partial-sum chunks consumed (parity of the part_full ring)
+    uint8_t* ystage = smem + C::kOffY + eh * 8192;
+    uint8_t* pstage = smem + C::kOffPart + eh * 16384;
+    uint64_t* pfull = part_full + 2 * eh;
+    uint32_t ych = 0;     // y staging chunks issued by this half
+    uint32_t pchunk = 0;  // partial-sum chunks consumed by this half (part_full parity)
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
     uint32_t seg = 0;
@@ -478,13 +486,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int n_tile = tile / p.tok_tiles;
       const int tok0 = (tile % p.tok_tiles) * NTOK;
       const int tvalid = (p.M - tok0) < NTOK ? (p.M - tok0) : NTOK;
-      // stage this tile's per-token scales while the MMAs run
-      named_bar_sync(1, kNumEpiWarps * 32);  // previous segment done reading sa_smem
-      for (int t = et; t < tvalid; t += kNumEpiWarps * 32) {
+      // stage this tile's per-token scales (and code sums) while the MMAs run
+      named_bar_sync(kBarAll, kAll);  // previous segment done reading sa_smem / rs_smem
+      for (int t = et; t < tvalid; t += kAll) {
         sa_smem[t] = p.s_a[tok0 + t];
         if constexpr (C::kU8) rs_smem[t] = 128 * p.rowsum[tok0 + t];
       }
-      named_bar_sync(1, kNumEpiWarps * 32);
+      named_bar_sync(kBarAll, kAll);
       const int n = n_tile * 128 + row;
       const bool n_ok = n < p.N;
       const bool whole = (kb0 == 0 && kb1 == p.kb_per_tile);
@@ -504,29 +512,30 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       mbar_wait(&acc_full[j], (seg / C::kAccBufs) & 1);
       tc_fence_after();
       if (lead && seg < 4) QQQ_STAMP(36 + 2 * seg);
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
+      const int nchunks = (tvalid + 15) / 16;
+      const int nmine = (nchunks - eh + 1) / 2;  // chunks c = eh, eh + 2, ...
       if (!owner) {
         // ---- contributor: red.add the partial into the tile's slot, release the counter
-        int32_t* slot = slots + row;
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
-        const int nchunks = (tvalid + 15) / 16;
 #pragma unroll 1
-        for (int c = 0; c < nchunks; ++c) {
+        for (int li = 0; li < nmine; ++li) {
+          const int c0 = (eh + 2 * li) * 16;
           uint32_t r[16];
-          tmem_ld16(taddr + c * 16, r);
+          tmem_ld16(taddr + c0, r);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            if (c * 16 + i < tvalid) red_add_s32(slot + (c * 16 + i) * 128, (int32_t)r[i]);
+            if (c0 + i < tvalid) red_add_s32(slots + (c0 + i) * 128 + row, (int32_t)r[i]);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[j]);
         __threadfence();
-        named_bar_sync(1, kNumEpiWarps * 32);
+        named_bar_sync(kBarAll, kAll);
         if (lead) atomicAdd(p.counters + tile, 1);
       } else {
         if (!whole) {
-          // ---- owner of a split tile: wait for the other nsegs-1 partials
+          // ---- owner of a split tile: wait for the other nsegs-1 contributions
           if (lead) {
             int32_t* cnt = p.counters + tile;
             int v;
@@ -535,46 +544,38 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             } while (v < nsegs - 1);
             *cnt = 0;  // re-arm for the next launch (every contributor has arrived)
           }
-          named_bar_sync(1, kNumEpiWarps * 32);
+          named_bar_sync(kBarAll, kAll);
         }
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
-        const int nchunks = (tvalid + 15) / 16;
         // reduced partial chunks [16 tok][128 rows] int32 (8 KiB, contiguous in the
-        // slot) are bulk-copied into a 2-deep smem ring, one chunk ahead
-        auto part_issue = [&](int c) {
-          const uint32_t pc = pchunk + c;
-          uint8_t* dst = smem + C::kOffPart + (pc & 1) * 8192;
-          mbar_arrive_expect_tx(&part_full[pc & 1], 8192);
-          bulk_g2s(dst, slots + (int64_t)c * 16 * 128, 8192, &part_full[pc & 1]);
+        // slot) are bulk-copied into this half's 2-deep smem ring, one chunk ahead
+        auto part_issue = [&](int li) {
+          const uint32_t pc = pchunk + li;
+          mbar_arrive_expect_tx(&pfull[pc & 1], 8192);
+          bulk_g2s(pstage + (pc & 1) * 8192, slots + (int64_t)(eh + 2 * li) * 16 * 128, 8192, &pfull[pc & 1]);
         };
-        if (!whole && lead) {
-          part_issue(0);
-          if (nchunks > 1) part_issue(1);
+        if (!whole && hlead) {
+          if (nmine > 0) part_issue(0);
+          if (nmine > 1) part_issue(1);
         }
 #pragma unroll 1
-        for (int c = 0; c < nchunks; ++c) {
-          const int c0 = c * 16;
+        for (int li = 0; li < nmine; ++li) {
+          const int c0 = (eh + 2 * li) * 16;
           uint32_t r[16];
           tmem_ld16(taddr + c0, r);
           tmem_wait_ld();
-          if (c + 1 == nchunks) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[j]);
-          }
-          if (lead && seg == 0 && c < 16) QQQ_STAMP(44 + c);
+          if (lead && seg == 0 && li < 16) QQQ_STAMP(44 + li);
           if (!whole) {
-            const uint32_t pc = pchunk + c;
-            mbar_wait(&part_full[pc & 1], (pc >> 1) & 1);
-            const int32_t* part = reinterpret_cast<const int32_t*>(smem + C::kOffPart + (pc & 1) * 8192);
+            const uint32_t pc = pchunk + li;
+            mbar_wait(&pfull[pc & 1], (pc >> 1) & 1);
+            const int32_t* part = reinterpret_cast<const int32_t*>(pstage + (pc & 1) * 8192);
 #pragma unroll
             for (int i = 0; i < 16; ++i) r[i] += (uint32_t)part[i * 128 + row];
             // return the slot to zero for the next launch (entries past tvalid were never touched)
 #pragma unroll
             for (int i = 0; i < 16; ++i)
               if (c0 + i < tvalid) __stcg(slots + (c0 + i) * 128 + row, 0);
-            named_bar_sync(1, kNumEpiWarps * 32);  // every thread has read this buffer
-            if (lead && c + 2 < nchunks) part_issue(c + 2);
+            named_bar_sync(kBarHalf, kHalf);  // this half has read the buffer
+            if (hlead && li + 2 < nmine) part_issue(li + 2);
           }
           if constexpr (C::kU8) {
 #pragma unroll
@@ -582,29 +583,32 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
           store_outputs(p, r, sa_smem + c0, tok0 + c0, tvalid - c0, n, n_ok, s_col);
           if (p.y_tma) {
-            // y tile chunk -> staging [16 tok][128 ch] fp16 -> one TMA store (OOB rows/cols clipped)
-            uint16_t* stg = reinterpret_cast<uint16_t*>(smem + C::kOffY + (ych & 1) * 4096);
-            if (lead) bulk_wait_read<1>();  // the store that used this buffer two chunks ago has read it
-            named_bar_sync(1, kNumEpiWarps * 32);
+            // y chunk -> staging [16 tok][128 ch] fp16 -> one TMA store (OOB rows/cols clipped)
+            uint16_t* stg = reinterpret_cast<uint16_t*>(ystage + (ych & 1) * 4096);
+            if (hlead) bulk_wait_read<1>();  // the store that used this buffer two chunks ago has read it
+            named_bar_sync(kBarHalf, kHalf);
             uint16_t h[16];
             dequant16(r, sa_smem + c0, s_col, h);
 #pragma unroll
             for (int i = 0; i < 16; ++i) stg[i * 128 + row] = h[i];
             fence_proxy_async_smem();
-            named_bar_sync(1, kNumEpiWarps * 32);
-            if (lead) {
+            named_bar_sync(kBarHalf, kHalf);
+            if (hlead) {
               tma_store_2d(&y_map, stg, n_tile * 128, tok0 + c0);
               bulk_commit();
             }
             ++ych;
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[j]);
+        if (!whole) pchunk += nmine;
       }
-      if (owner && !whole) pchunk += (tvalid + 15) / 16;
       if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
       ++seg;
     }
-    if (lead) bulk_wait_all();  // y stores complete before the CTA retires
+    if (hlead) bulk_wait_all();  // y stores complete before the CTA retires
   }
 
   __syncthreads();
