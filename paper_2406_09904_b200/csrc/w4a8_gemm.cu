@@ -686,8 +686,10 @@ static LaunchPlan plan_for(int64_t M, int64_t N, int64_t K, int ntok, bool strea
 // (scripts/quick_bench.py tile-plan sweeps, profiles/README.md):
 //   T = T0 + units_per_CTA * max(weight bytes / per-CTA HBM share, MMA time,
 //       activation smem traffic) + split-K fix-up + last-tile epilogue.
-static double plan_cost_us(const LaunchPlan& lp) {
-  const double T0 = 1.15, kBsm = 19.6e3, kBtot = 2953e3, kF0 = 4.69, kF1 = 0.046, kE1 = 0.045, kMma = 0.91;
+static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
+  // fitted (log-least-squares) on profiles/r01_tileplan_sweep.jsonl, per-group g=128
+  const double T0 = 2.47, kBsm = 250.7e3, kBtot = 3136e3, kF0 = 2.80, kF1 = 0.0135, kE1 = 0.0349, kMma = 1.77,
+               kConv = 0.02419e-3;  // us per weight per CTA
   const double clk = 1900.0;  // MHz
   const int64_t ucta = lp.aligned_tiles > 0 ? (int64_t)lp.aligned_tiles * lp.kb_per_tile
                                             : (lp.units + lp.grid - 1) / lp.grid;
@@ -695,9 +697,10 @@ static double plan_cost_us(const LaunchPlan& lp) {
   const double wkb = lp.bk * 64.0 * (1.0 + 1.0 / 32);
   const double mma = (lp.bk / 32.0) * (lp.ntok / 2.0) / clk * kMma;
   const double act = 2.0 * lp.ntok * lp.bk / 128.0 / clk;
-  const double u = std::max(wkb / bw, std::max(mma, act));
+  const double conv = lp.bk * 128.0 * kConv;
+  const double u = std::max(std::max(wkb / bw, conv), std::max(mma, act));
   const double fix = lp.aligned_tiles > 0 ? 0.0 : kF0 + kF1 * lp.ntok;
-  return T0 + ucta * u + fix + kE1 * lp.ntok;
+  return T0 + ucta * u + fix + kE1 * (double)std::min<int64_t>(lp.ntok, M);
 }
 
 static LaunchPlan make_plan(int64_t M, int64_t N, int64_t K, int force_ntok, int force_grid, int force_split) {
@@ -713,7 +716,7 @@ static LaunchPlan make_plan(int64_t M, int64_t N, int64_t K, int force_ntok, int
     for (int sk = 0; sk < 2; ++sk) {
       const LaunchPlan lp = plan_for(M, N, K, nt, sk == 1, 0);
       if (lp.tiles > 65536) continue;
-      const double t = plan_cost_us(lp);
+      const double t = plan_cost_us(lp, M);
       if (t < best_t) {
         best_t = t;
         best = lp;
