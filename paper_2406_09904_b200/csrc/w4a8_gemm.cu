@@ -38,7 +38,7 @@
 
 namespace qqq {
 
-constexpr int kNumConvWarps = 8;
+constexpr int kNumConvWarps = 16;  // 4 per TMEM lane quadrant
 constexpr int kConvWarp0 = 0;
 constexpr int kEpiWarp0 = kNumConvWarps, kNumEpiWarps = 8;  // two halves of 4 (one per TMEM lane quadrant)
 constexpr int kAllocWarp = kEpiWarp0 + kNumEpiWarps;
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // Warp w owns TMEM lane quadrant q = w % 4 (rows 32q..32q+31) and every
     // other 32-k slab (parity w / 4): thread = one output channel.
     if constexpr (C::kConvert) {
-      const int q = warp & 3, h = (warp >> 2) & 1;
+      const int q = warp & 3, h = warp >> 2;  // quadrant, slab phase (0..kConvPhases-1)
       const int row = q * 32 + lane;
       const int geff = p.group < 128 ? p.group : 128;
       uint32_t magic;
@@ -400,7 +400,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       SegIter si = make_iter(p);
       int tile, kb0, kb1;
       uint32_t it = 0;
-      constexpr int kSlabs = BK / 32 / 2;  // slabs per warp per k-block
+      constexpr int kPhases = kNumConvWarps / 4;
+      constexpr int kSlabs = BK / 32 / kPhases;  // slabs per warp per k-block
       while (si.next(tile, kb0, kb1)) {
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::kWStages;
@@ -411,7 +412,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           __half s1[kSlabs];
 #pragma unroll
           for (int i = 0; i < kSlabs; ++i) {  // all shared loads first (ILP)
-            const int c = h + 2 * i;
+            const int c = h + kPhases * i;
             const uint8_t* ssp = wst + (c >> 2) * p.ss_bytes;
             v[i] = *reinterpret_cast<const uint4*>(ssp + ((c & 3) * 128 + row) * 16);
             if constexpr (MODE == kModePG)
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           tc_fence_after();
           if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(64 + it);
 #pragma unroll
-          for (int i = 0; i < kSlabs; ++i) tmem_st8(a_lane + b * C::kACols + (h + 2 * i) * 8, o[i]);
+          for (int i = 0; i < kSlabs; ++i) tmem_st8(a_lane + b * C::kACols + (h + kPhases * i) * 8, o[i]);
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
