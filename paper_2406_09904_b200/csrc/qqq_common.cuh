@@ -102,6 +102,29 @@ QQQ_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Parity wait for roles that idle for long stretches (epilogue, producers):
+// the try_wait carries a suspend-time hint, so the warp sleeps in hardware
+// until the phase completes instead of re-issuing the poll loop at high warp
+// priority and stealing issue slots from the converter warps.
+QQQ_DEVICE void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+#pragma unroll 1
+  for (uint32_t n = 0;; ++n) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity), "r"(0x100000u)
+        : "memory");
+    if (done) return;
+#ifndef QQQ_NO_WATCHDOG
+    if (n > (1u << 22)) __trap();
+#endif
+  }
+}
+
 // ----------------------------------------------------------------------------
 // TMA / bulk copies (async proxy)
 // ----------------------------------------------------------------------------

@@ -47,7 +47,9 @@ constexpr int kWProducerWarp = kAllocWarp + 2;
 constexpr int kMmaWarp = kAllocWarp + 3;
 constexpr int kNumThreads = (kMmaWarp + 1) * 32;
 constexpr int kSmemBudget = 225 * 1024;
+#ifdef QQQ_TIMELINE
 constexpr int kDbgSlots = 128;
+#endif
 
 struct GemmParams {
   const uint8_t* w;     // repacked weight blob (qqq_layout.cuh)
@@ -124,10 +126,18 @@ QQQ_DEVICE unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// In-kernel timeline stamps exist only in the developer build (-DQQQ_TIMELINE,
+// libqqq_b200_tl.so); the product build carries no instrumentation code.
+#ifdef QQQ_TIMELINE
 #define QQQ_STAMP(slot)                                                   \
   do {                                                                    \
     if (p.dbg) p.dbg[(size_t)blockIdx.x * kDbgSlots + (slot)] = gtimer(); \
   } while (0)
+#else
+#define QQQ_STAMP(slot) \
+  do {                  \
+  } while (0)
+#endif
 
 // Programmatic dependent launch (PDL). No-ops without the launch attribute.
 QQQ_DEVICE void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -294,79 +304,93 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // The single-issuer roles (producers, MMA) run their loops with the whole
+  // warp converged and elect one lane per async instruction: the operands are
+  // then warp-uniform and live in uniform registers. Issuing tcgen05.mma from
+  // a divergent single lane costs ~150 cycles per MMA (R2UR waterfall,
+  // scripts/mma_probe.cu) against a 16-cycle issue floor at N = 16.
   if (warp == kWProducerWarp) {
     // ===================== weight producer (bulk copies) =====================
     // Weights never depend on the previous kernel in the stream: no PDL wait,
     // so under PDL they stream in while the previous kernel drains.
-    if (lane == 0) {
-      QQQ_STAMP(1);
-      const uint32_t wbytes = (uint32_t)((BK / 128) * p.ss_bytes);
-      SegIter si = make_iter(p);
-      int tile, kb0, kb1;
-      uint32_t it = 0;
-      while (si.next(tile, kb0, kb1)) {
-        const int n_tile = tile / p.tok_tiles;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % C::kWStages;
-          mbar_wait(&w_empty[s], ((it / C::kWStages) & 1) ^ 1);
+    if (lane == 0) QQQ_STAMP(1);
+    const uint32_t wbytes = (uint32_t)((BK / 128) * p.ss_bytes);
+    SegIter si = make_iter(p);
+    int tile, kb0, kb1;
+    uint32_t s = 0, ph = 0;
+    while (si.next(tile, kb0, kb1)) {
+      const int n_tile = tile / p.tok_tiles;
+#pragma unroll 1
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait_sleep(&w_empty[s], ph ^ 1);
+        if (elect_one()) {
           mbar_arrive_expect_tx(&w_full[s], wbytes);
           const int64_t ss0 = (int64_t)n_tile * p.ss_per_tile + (int64_t)kb * (BK / 128);
           bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &w_full[s]);
         }
+        __syncwarp();
+        if (++s == C::kWStages) {
+          s = 0;
+          ph ^= 1;
+        }
       }
-      QQQ_STAMP(2);
     }
+    if (lane == 0) QQQ_STAMP(2);
   } else if (warp == kActProducerWarp) {
     // ================== activation producer (3-D tensor TMA) ==================
-    if (lane == 0) {
-      griddep_wait();  // the int8 activations come from the previous kernel
-      QQQ_STAMP(3);
-      SegIter si = make_iter(p);
-      int tile, kb0, kb1;
-      uint32_t it = 0;
-      while (si.next(tile, kb0, kb1)) {
-        const int tok0 = (tile % p.tok_tiles) * NTOK;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % C::kXStages;
-          mbar_wait(&x_empty[s], ((it / C::kXStages) & 1) ^ 1);
+    griddep_wait();  // the int8 activations come from the previous kernel
+    if (lane == 0) QQQ_STAMP(3);
+    SegIter si = make_iter(p);
+    int tile, kb0, kb1;
+    uint32_t s = 0, ph = 0;
+    while (si.next(tile, kb0, kb1)) {
+      const int tok0 = (tile % p.tok_tiles) * NTOK;
+#pragma unroll 1
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait_sleep(&x_empty[s], ph ^ 1);
+        if (elect_one()) {
           mbar_arrive_expect_tx(&x_full[s], C::kXBytes);
           tma_load_3d(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0, kb * (BK / 128), &x_full[s]);
+        }
+        __syncwarp();
+        if (++s == C::kXStages) {
+          s = 0;
+          ph ^= 1;
         }
       }
     }
   } else if (warp == kMmaWarp) {
     // ============================ MMA issuer ============================
-    if (lane == 0) {
-      SegIter si = make_iter(p);
-      int tile, kb0, kb1;
-      uint32_t it = 0, seg = 0;
-      while (si.next(tile, kb0, kb1)) {
-        const int j = seg % C::kAccBufs;
-        mbar_wait(&acc_empty[j], ((seg / C::kAccBufs) & 1) ^ 1);
+    SegIter si = make_iter(p);
+    int tile, kb0, kb1;
+    uint32_t it = 0, seg = 0;
+    uint32_t xs = 0, xph = 0, b = 0, bph = 0, j = 0, jph = 0;
+    while (si.next(tile, kb0, kb1)) {
+      mbar_wait_sleep(&acc_empty[j], jph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + j * NTOK;
+#pragma unroll 1
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        mbar_wait_sleep(&x_full[xs], xph);
+        if (lane == 0 && it < 16) QQQ_STAMP(96 + it);
+        uint32_t a_addr;
+        if constexpr (C::kConvert) {
+          mbar_wait_sleep(&a_full[b], bph);
+          if (lane == 0 && it < 16) QQQ_STAMP(112 + it);
+          a_addr = tmem_base + C::kAccCols + b * C::kACols;  // TMEM column address
+        } else {
+          mbar_wait_sleep(&w_full[b], bph);
+          a_addr = smem_u32(smem + C::kOffW + b * C::kWBytes);
+        }
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + j * NTOK;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int xs = it % C::kXStages;
-          mbar_wait(&x_full[xs], (it / C::kXStages) & 1);
-          uint32_t a_addr;
-          int b = 0, ws = 0;
-          if constexpr (C::kConvert) {
-            b = it % C::kABufs;
-            mbar_wait(&a_full[b], (it / C::kABufs) & 1);
-            a_addr = tmem_base + C::kAccCols + b * C::kACols;  // TMEM column address
-          } else {
-            ws = it % C::kWStages;
-            mbar_wait(&w_full[ws], (it / C::kWStages) & 1);
-            a_addr = smem_u32(smem + C::kOffW + ws * C::kWBytes);
-          }
-          tc_fence_after();
-          const uint32_t act_addr = smem_u32(smem + C::kOffX + xs * C::kXBytes);
+        const uint32_t act_addr = smem_u32(smem + C::kOffX + xs * C::kXBytes);
 #pragma unroll
-          for (int kk = 0; kk < BK / 32; ++kk) {
-            // B: SWIZZLE_128B [k-atom][NTOK rows][128 B]; 32 B K-steps inside the atom
-            const uint32_t b_addr = act_addr + (kk / 4) * (NTOK * 128) + (kk % 4) * 32;
-            const uint64_t b_desc = make_smem_desc(b_addr, 16, 1024, 2);
-            const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
+        for (int kk = 0; kk < BK / 32; ++kk) {
+          // B: SWIZZLE_128B [k-atom][NTOK rows][128 B]; 32 B K-steps inside the atom
+          const uint32_t b_addr = act_addr + (kk / 4) * (NTOK * 128) + (kk % 4) * 32;
+          const uint64_t b_desc = make_smem_desc(b_addr, 16, 1024, 2);
+          const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
+          if (elect_one()) {
             if constexpr (C::kConvert) {
               mma_i8_ts(d_tmem, a_addr + kk * 8, b_desc, C::kIdesc, acc);  // A: 8 TMEM columns per K=32
             } else {
@@ -374,49 +398,81 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               mma_i8_ss(d_tmem, make_smem_desc(a_addr + kk * 2 * 2048, 2048, 128, 0), b_desc, C::kIdesc, acc);
             }
           }
+          __syncwarp();
+        }
+        if (elect_one()) {
           mma_commit(&x_empty[xs]);
-          if (it < 16) QQQ_STAMP(20 + it);
           if constexpr (C::kConvert) {
             mma_commit(&a_empty[b]);
           } else {
-            mma_commit(&w_empty[ws]);
+            mma_commit(&w_empty[b]);
           }
         }
-        mma_commit(&acc_full[j]);
-        ++seg;
+        __syncwarp();
+        if (lane == 0 && it < 16) QQQ_STAMP(20 + it);
+        if (++xs == C::kXStages) {
+          xs = 0;
+          xph ^= 1;
+        }
+        if (++b == (C::kConvert ? (uint32_t)C::kABufs : (uint32_t)C::kWStages)) {
+          b = 0;
+          bph ^= 1;
+        }
       }
+      if (elect_one()) mma_commit(&acc_full[j]);
+      __syncwarp();
+      if (++j == C::kAccBufs) {
+        j = 0;
+        jph ^= 1;
+      }
+      ++seg;
     }
   } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kNumConvWarps) {
     // ====================== INT4 -> INT8 converters ======================
     // Warp w owns TMEM lane quadrant q = w % 4 (rows 32q..32q+31) and every
     // other 32-k slab (parity w / 4): thread = one output channel.
     if constexpr (C::kConvert) {
-      const int q = warp & 3, h = warp >> 2;  // quadrant, slab phase (0..kConvPhases-1)
+      const int q = warp & 3, h = warp >> 2;  // quadrant, slab phase (0..kPhases-1)
       const int row = q * 32 + lane;
-      const int geff = p.group < 128 ? p.group : 128;
-      uint32_t magic;
-      asm("mov.b32 %0, 0x64006400;" : "=r"(magic));  // a register operand for the fused and-or lop3
-      const uint32_t a_lane = tmem_base + ((uint32_t)(q * 32) << 16) + C::kAccCols;
-      SegIter si = make_iter(p);
-      int tile, kb0, kb1;
-      uint32_t it = 0;
       constexpr int kPhases = kNumConvWarps / 4;
       constexpr int kSlabs = BK / 32 / kPhases;  // slabs per warp per k-block
+      uint32_t magic;
+      asm("mov.b32 %0, 0x64006400;" : "=r"(magic));  // a register operand for the fused and-or lop3
+      // loop-invariant shared-memory offsets (inside a weight stage) of this
+      // thread's packed slabs and group scales, and its TMEM column offsets
+      uint32_t voff[kSlabs], soff[kSlabs];
+      {
+        const int geff = p.group < 128 ? p.group : 128;
+#pragma unroll
+        for (int i = 0; i < kSlabs; ++i) {
+          const int c = h + kPhases * i;
+          voff[i] = (uint32_t)((c >> 2) * p.ss_bytes + ((c & 3) * 128 + row) * 16);
+          soff[i] = (uint32_t)((c >> 2) * p.ss_bytes + 8192 + ((((c & 3) * 32) / geff) * 128 + row) * 2);
+        }
+      }
+      const uint32_t a_lane = tmem_base + ((uint32_t)(q * 32) << 16) + C::kAccCols + h * 8;
+      const uint32_t wst0 = smem_u32(smem + C::kOffW);
+      SegIter si = make_iter(p);
+      int tile, kb0, kb1;
+      uint32_t ws = 0, wph = 0, ab = 0, aph = 0, it = 0;
       while (si.next(tile, kb0, kb1)) {
+#pragma unroll 1
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % C::kWStages;
-          mbar_wait(&w_full[s], (it / C::kWStages) & 1);
+          mbar_wait(&w_full[ws], wph);
           if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(4 + it);
-          const uint8_t* wst = smem + C::kOffW + s * C::kWBytes;
+          const uint32_t wst = wst0 + ws * C::kWBytes;
           uint4 v[kSlabs];
-          __half s1[kSlabs];
+          uint32_t s1[kSlabs];
 #pragma unroll
           for (int i = 0; i < kSlabs; ++i) {  // all shared loads first (ILP)
-            const int c = h + kPhases * i;
-            const uint8_t* ssp = wst + (c >> 2) * p.ss_bytes;
-            v[i] = *reinterpret_cast<const uint4*>(ssp + ((c & 3) * 128 + row) * 16);
-            if constexpr (MODE == kModePG)
-              s1[i] = reinterpret_cast<const __half*>(ssp + 8192)[(((c & 3) * 32) / geff) * 128 + row];
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v[i].x), "=r"(v[i].y), "=r"(v[i].z), "=r"(v[i].w)
+                         : "r"(wst + voff[i]));
+            if constexpr (MODE == kModePG) {
+              uint16_t sv;
+              asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sv) : "r"(wst + soff[i]));
+              s1[i] = sv;
+            }
           }
           uint32_t o[kSlabs][8];
 #pragma unroll
@@ -427,7 +483,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               pc_convert_word(v[i].z, o[i][2], o[i][6]);
               pc_convert_word(v[i].w, o[i][3], o[i][7]);
             } else {
-              const __half2 s2 = __halves2half2(s1[i], s1[i]);
+              const __half2 s2 = u32_as_h2(s1[i] | (s1[i] << 16));
               const __half2 s16 = __hmul2(s2, u32_as_h2(0x2C002C00u));  // * 1/16
               pg_convert_word<false, true>(v[i].x, s2, s16, magic, o[i][0], o[i][1]);
               pg_convert_word<false, true>(v[i].y, s2, s16, magic, o[i][2], o[i][3]);
@@ -435,19 +491,27 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               pg_convert_word<false, true>(v[i].w, s2, s16, magic, o[i][6], o[i][7]);
             }
           }
-          // the packed stage is consumed (values are in registers): release it now
+          // the packed stage is consumed (the converted values are in registers): release it
           __syncwarp();
-          if (lane == 0) mbar_arrive(&w_empty[s]);
-          const int b = it % C::kABufs;
-          mbar_wait(&a_empty[b], ((it / C::kABufs) & 1) ^ 1);
+          if (lane == 0) mbar_arrive(&w_empty[ws]);
+          if (++ws == C::kWStages) {
+            ws = 0;
+            wph ^= 1;
+          }
+          mbar_wait(&a_empty[ab], aph ^ 1);
           tc_fence_after();
           if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(64 + it);
+          const uint32_t abase = a_lane + ab * C::kACols;
 #pragma unroll
-          for (int i = 0; i < kSlabs; ++i) tmem_st8(a_lane + b * C::kACols + (h + kPhases * i) * 8, o[i]);
+          for (int i = 0; i < kSlabs; ++i) tmem_st8(abase + kPhases * i * 8, o[i]);
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&a_full[b]);
+          if (lane == 0) mbar_arrive(&a_full[ab]);
+          if (++ab == C::kABufs) {
+            ab = 0;
+            aph ^= 1;
+          }
           if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(80 + it);
         }
       }
@@ -510,7 +574,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       }
       const bool owner = whole || seg_idx == 0;
       const int j = seg % C::kAccBufs;
-      mbar_wait(&acc_full[j], (seg / C::kAccBufs) & 1);
+      mbar_wait_sleep(&acc_full[j], (seg / C::kAccBufs) & 1);
       tc_fence_after();
       if (lead && seg < 4) QQQ_STAMP(36 + 2 * seg);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;

@@ -36,7 +36,8 @@ def main():
                 R = 2
             reps = [prep] + [G.PreparedWeights(prep.mode, prep.w.clone(), None if prep.sc is None else prep.sc.clone(),
                                                prep.group, prep.s_col.clone()) for _ in range(R - 1)]
-            w16 = [torch.randn((k, n), dtype=torch.float16, device=dev) for _ in range(2)] if a.fp16 else None
+            r16 = max(2, math.ceil(2.5 * B.L2_BYTES / (k * n * 2)))
+            w16 = [torch.randn((k, n), dtype=torch.float16, device=dev) for _ in range(r16)] if a.fp16 else None
             for m in map(int, a.ms.split(",")):
                 x = torch.randn((m, k), dtype=torch.float16, device=dev)
                 aq = Q.quant_act_per_token(x)
@@ -56,7 +57,8 @@ def main():
                     rec = dict(shape=shp, scheme=scheme, M=m, cfg=cfg, us=round(t, 2), TOPS=round(ops / t / 1e6, 1),
                                GBps=round(byt / t / 1e3, 1), roof_frac=round(roof / t, 3))
                     if w16:
-                        t16 = B.graph_time_us([(lambda wi: (lambda: torch.matmul(x, wi)))(wi) for wi in w16], reps=20)
+                        t16 = B.graph_time_us([(lambda wi: (lambda: torch.matmul(x, wi)))(wi) for wi in w16],
+                                              reps=max(2, 40 // len(w16)))
                         rec["fp16_us"] = round(t16, 2)
                         rec["speedup"] = round(t16 / t, 2)
                     print(json.dumps(rec), flush=True)

@@ -1,5 +1,6 @@
 """Per-CTA in-kernel timeline (%globaltimer stamps) of one W4A8 GEMM launch."""
 import argparse, json, os, sys
+os.environ["QQQ_TIMELINE_LIB"] = "1"  # the instrumented developer build (build.py --timeline)
 import numpy as np
 import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -12,6 +13,8 @@ NAMES = {0: "start", 1: "setup", 2: "w_issued", 3: "dep_wait", 63: "end"}
 for i in range(16):
     NAMES[4 + i] = f"full{i}"
     NAMES[20 + i] = f"mma{i}"
+    NAMES[96 + i] = f"mma_xfull{i}"
+    NAMES[112 + i] = f"mma_afull{i}"
 for c in range(16):
     NAMES[44 + c] = f"epi0_c{c}"
     NAMES[64 + c] = f"conv_ae{c}"
