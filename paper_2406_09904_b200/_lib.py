@@ -16,6 +16,7 @@ from .errors import ConfigError, CorruptionError, DataError, KernelError, ShapeE
 # QQQ_TIMELINE_LIB=1 selects the developer build with in-kernel timeline stamps
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
                         "libqqq_b200_tl.so" if os.environ.get("QQQ_TIMELINE_LIB") == "1" else "libqqq_b200.so")
+LIB_PATH = os.environ.get("QQQ_LIB_PATH", LIB_PATH)  # developer A/B builds (scripts/)
 
 QQQ_OK, QQQ_ERR_SHAPE, QQQ_ERR_DATA, QQQ_ERR_CONFIG, QQQ_ERR_CORRUPTION, QQQ_ERR_CUDA, QQQ_ERR_UNSUPPORTED = range(7)
 STAT_NONFINITE, STAT_CODE_RANGE, STAT_PAD_NIBBLE, STAT_SCALE_INF, STAT_NEED_CLAMP, STAT_TINY_SCALE = 1, 2, 4, 8, 16, 32

@@ -50,13 +50,17 @@ def up_to_date(lib: str = LIB) -> bool:
     return all(os.path.getmtime(f) <= t for f in _deps())
 
 
-def build_library(force: bool = False, verbose: bool = False, timeline: bool = False) -> str:
+def build_library(force: bool = False, verbose: bool = False, timeline: bool = False, defines=(), name=None) -> str:
+    """Build the product library (or, for developer A/B runs, a variant with
+    extra -D defines written to lib/<name>.so)."""
     lib = LIB_TL if timeline else LIB
+    if name:
+        lib = os.path.join(LIBDIR, name + ".so")
     if not force and up_to_date(lib):
         return lib
     nvcc = _nvcc()
-    objdir = os.path.join(PKG, "build", "tl" if timeline else "prod")
-    extra = ["-DQQQ_TIMELINE"] if timeline else []
+    objdir = os.path.join(PKG, "build", name or ("tl" if timeline else "prod"))
+    extra = (["-DQQQ_TIMELINE"] if timeline else []) + ["-D" + d for d in defines]
     os.makedirs(objdir, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
 
@@ -84,4 +88,7 @@ def build_library(force: bool = False, verbose: bool = False, timeline: bool = F
 
 
 if __name__ == "__main__":
-    print(build_library(force="--force" in sys.argv, verbose=True, timeline="--timeline" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    names = [a[7:] for a in sys.argv[1:] if a.startswith("--name=")]
+    print(build_library(force="--force" in sys.argv, verbose=True, timeline="--timeline" in sys.argv, defines=defs,
+                        name=names[0] if names else None))

@@ -48,7 +48,7 @@ constexpr int kMmaWarp = kAllocWarp + 3;
 constexpr int kNumThreads = (kMmaWarp + 1) * 32;
 constexpr int kSmemBudget = 225 * 1024;
 #ifdef QQQ_TIMELINE
-constexpr int kDbgSlots = 128;
+constexpr int kDbgSlots = 192;
 #endif
 
 struct GemmParams {
@@ -73,9 +73,12 @@ struct GemmParams {
 template <int MODE, int NTOK, int BK>
 struct Cfg {
   static constexpr bool kConvert = MODE != kModeI8;
-  // two independent TMA rings: weights (released by the converters right after
-  // their shared-memory loads, or by the MMA in I8 mode) and activations
-  // (released by the MMA)
+  // Two rings. Weights: their own TMA ring (released by the converters once
+  // the packed bytes are consumed, or by the MMA in I8 mode). K-blocks: ring
+  // slot s = activation stage s = TMEM A buffer s, guarded by ONE full barrier
+  // (activation TMA bytes + one arrival per converter warp + the producer's
+  // arrive) and ONE empty barrier (the MMA's commit), so the MMA warp pays one
+  // wait and one commit per k-block (each ~130 cycles, scripts/mma_probe2.cu).
   static constexpr int kXBytes = NTOK * BK;
   static constexpr int kSSMax = MODE == kModeI8 ? 16384 : MODE == kModePC ? 8192 : 8192 + 256 * 4;
   static constexpr int kWBytes = (BK / 128) * kSSMax;  // worst case (PG, g = 32)
@@ -83,23 +86,24 @@ struct Cfg {
   // kABufs buffers of BK/4 columns (128 lanes x 4 int8 per column). This keeps
   // the 1 B/weight operand off the shared-memory crossbar, which otherwise
   // bounds the decode stream (TMA write + STS + MMA read of every weight).
-  static constexpr int kABufs = kConvert ? 4 : 0;
   static constexpr int kACols = BK / 4;
   static constexpr int kAccBufs = NTOK == 256 ? 1 : 2;
   static constexpr int kAccCols = kAccBufs * NTOK;
+  static constexpr int kABufsMax = kConvert ? (512 - kAccCols) / kACols : 8;
   static constexpr int kRingBudget = kSmemBudget - 4096 - NTOK * 12 - 2 * 2 * 16 * 256 - 2 * 2 * 8192;
-  // activations get what is left after >= 4 weight stages (capped at 8): small
-  // for decode tiles, and deep enough at large NTOK that the L2->smem latency of
-  // a 32 KiB activation tile is hidden
-  static constexpr int kXStagesRaw = (kRingBudget - 4 * kWBytes) / kXBytes;
-  static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > 8 ? 8 : kXStagesRaw);
+  // k-block ring depth: what is left after 3 weight stages, at most 4 and at
+  // most the number of TMEM A buffers that fit beside the accumulators
+  static constexpr int kXStagesRaw = (kRingBudget - 3 * kWBytes) / kXBytes;
+  static constexpr int kXCap = kABufsMax < 4 ? kABufsMax : 4;
+  static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > kXCap ? kXCap : kXStagesRaw);
+  static constexpr int kABufs = kConvert ? kXStages : 0;
   static constexpr int kWStagesRaw = (kRingBudget - kXStages * kXBytes) / kWBytes;
   static constexpr int kWStages = kWStagesRaw > 12 ? 12 : kWStagesRaw;
   static_assert(kWStages >= 2, "shared memory budget too small");
   static constexpr int kOffX = 0;  // 1024-aligned: NTOK*BK is a multiple of 2048
   static constexpr int kOffW = kOffX + kXStages * kXBytes;
   static constexpr int kOffBar = (kOffW + kWStages * kWBytes + 1023) / 1024 * 1024;
-  static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 2 * kABufs + 4 + 4;
+  static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 4 + 4;
   static constexpr int kOffSA = kOffBar + (kNumBars * 8 + 16 + 15) / 16 * 16;  // per-token scales of a tile (f64)
   static constexpr int kOffRS = kOffSA + NTOK * 8;                             // per-token code sums (int32)
   static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;  // per epilogue half: 2 x [16 tok][128 ch] fp16
@@ -137,6 +141,17 @@ QQQ_DEVICE unsigned long long gtimer() {
 #define QQQ_STAMP(slot) \
   do {                  \
   } while (0)
+#endif
+
+#ifdef QQQ_CONV_SLEEP
+#define conv_wait mbar_wait_sleep
+#else
+#define conv_wait mbar_wait
+#endif
+#ifdef QQQ_MMA_SPIN
+#define mma_wait mbar_wait
+#else
+#define mma_wait mbar_wait_sleep
 #endif
 
 // Programmatic dependent launch (PDL). No-ops without the launch attribute.
@@ -261,13 +276,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
-  uint64_t* x_full = bars;
-  uint64_t* x_empty = x_full + C::kXStages;
-  uint64_t* w_full = x_empty + C::kXStages;
+  uint64_t* kb_full = bars;                   // [kXStages] activations landed + A buffer converted
+  uint64_t* kb_empty = kb_full + C::kXStages;  // [kXStages] MMA done with activation stage / A buffer
+  uint64_t* w_full = kb_empty + C::kXStages;
   uint64_t* w_empty = w_full + C::kWStages;
-  uint64_t* a_full = w_empty + C::kWStages;
-  uint64_t* a_empty = a_full + C::kABufs;
-  uint64_t* acc_full = a_empty + C::kABufs;
+  uint64_t* acc_full = w_empty + C::kWStages;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* part_full = acc_empty + 2;  // [half][2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
@@ -279,16 +292,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     QQQ_STAMP(0);
     griddep_launch_dependents();
     for (int s = 0; s < C::kXStages; ++s) {
-      mbar_init(&x_full[s], 1);
-      mbar_init(&x_empty[s], 1);
+      mbar_init(&kb_full[s], C::kConvert ? kNumConvWarps + 1 : 1);
+      mbar_init(&kb_empty[s], 1);
     }
     for (int s = 0; s < C::kWStages; ++s) {
       mbar_init(&w_full[s], 1);
       mbar_init(&w_empty[s], C::kConvert ? kNumConvWarps : 1);
-    }
-    for (int b = 0; b < C::kABufs; ++b) {
-      mbar_init(&a_full[b], kNumConvWarps);
-      mbar_init(&a_empty[b], 1);
     }
     for (int j = 0; j < C::kAccBufs; ++j) {
       mbar_init(&acc_full[j], 1);
@@ -314,7 +323,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // Weights never depend on the previous kernel in the stream: no PDL wait,
     // so under PDL they stream in while the previous kernel drains.
     if (lane == 0) QQQ_STAMP(1);
-    const uint32_t wbytes = (uint32_t)((BK / 128) * p.ss_bytes);
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
     uint32_t s = 0, ph = 0;
@@ -324,6 +332,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait_sleep(&w_empty[s], ph ^ 1);
         if (elect_one()) {
+          // the last k-block of a tile may hold fewer super-slabs (K_pad % BK != 0):
+          // the stale rest of the stage meets zero-filled (OOB) activations
+          const int nss = min(BK / 128, p.ss_per_tile - kb * (BK / 128));
+          const uint32_t wbytes = (uint32_t)(nss * p.ss_bytes);
           mbar_arrive_expect_tx(&w_full[s], wbytes);
           const int64_t ss0 = (int64_t)n_tile * p.ss_per_tile + (int64_t)kb * (BK / 128);
           bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &w_full[s]);
@@ -347,10 +359,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int tok0 = (tile % p.tok_tiles) * NTOK;
 #pragma unroll 1
       for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait_sleep(&x_empty[s], ph ^ 1);
+        mbar_wait_sleep(&kb_empty[s], ph ^ 1);
         if (elect_one()) {
-          mbar_arrive_expect_tx(&x_full[s], C::kXBytes);
-          tma_load_3d(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0, kb * (BK / 128), &x_full[s]);
+          mbar_arrive_expect_tx(&kb_full[s], C::kXBytes);
+          tma_load_3d(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0, kb * (BK / 128), &kb_full[s]);
         }
         __syncwarp();
         if (++s == C::kXStages) {
@@ -364,49 +376,37 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
     uint32_t it = 0, seg = 0;
-    uint32_t xs = 0, xph = 0, b = 0, bph = 0, j = 0, jph = 0;
+    uint32_t xs = 0, xph = 0, ws = 0, wph = 0, j = 0, jph = 0;
     while (si.next(tile, kb0, kb1)) {
       mbar_wait_sleep(&acc_empty[j], jph ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + j * NTOK;
 #pragma unroll 1
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
-        mbar_wait_sleep(&x_full[xs], xph);
+        mma_wait(&kb_full[xs], xph);  // activations landed and (convert modes) the A buffer is converted
         if (lane == 0 && it < 16) QQQ_STAMP(96 + it);
-        uint32_t a_addr;
-        if constexpr (C::kConvert) {
-          mbar_wait_sleep(&a_full[b], bph);
-          if (lane == 0 && it < 16) QQQ_STAMP(112 + it);
-          a_addr = tmem_base + C::kAccCols + b * C::kACols;  // TMEM column address
-        } else {
-          mbar_wait_sleep(&w_full[b], bph);
-          a_addr = smem_u32(smem + C::kOffW + b * C::kWBytes);
-        }
+        if constexpr (!C::kConvert) mma_wait(&w_full[ws], wph);
         tc_fence_after();
         const uint32_t act_addr = smem_u32(smem + C::kOffX + xs * C::kXBytes);
+        const uint64_t b_desc0 = make_smem_desc(act_addr, 16, 1024, 2);
+        const uint32_t a_tmem = tmem_base + C::kAccCols + xs * C::kACols;  // TMEM column address (convert modes)
+        const uint32_t a_smem = smem_u32(smem + C::kOffW + ws * C::kWBytes);  // I8 mode
+        const uint32_t acc0 = kb > kb0 ? 1u : 0u;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BK / 32; ++kk) {
-          // B: SWIZZLE_128B [k-atom][NTOK rows][128 B]; 32 B K-steps inside the atom
-          const uint32_t b_addr = act_addr + (kk / 4) * (NTOK * 128) + (kk % 4) * 32;
-          const uint64_t b_desc = make_smem_desc(b_addr, 16, 1024, 2);
-          const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
-          if (elect_one()) {
+          for (int kk = 0; kk < BK / 32; ++kk) {
+            // B: SWIZZLE_128B [k-atom][NTOK rows][128 B]; 32 B K-steps inside the atom
+            const uint64_t b_desc = b_desc0 + (uint64_t)(((kk / 4) * (NTOK * 128) + (kk % 4) * 32) >> 4);
+            const uint32_t acc = kk > 0 ? 1u : acc0;
             if constexpr (C::kConvert) {
-              mma_i8_ts(d_tmem, a_addr + kk * 8, b_desc, C::kIdesc, acc);  // A: 8 TMEM columns per K=32
+              mma_i8_ts(d_tmem, a_tmem + kk * 8, b_desc, C::kIdesc, acc);  // A: 8 TMEM columns per K=32
             } else {
               // A: canonical K-major, no swizzle: [k16 chunk][128 rows][16 B]
-              mma_i8_ss(d_tmem, make_smem_desc(a_addr + kk * 2 * 2048, 2048, 128, 0), b_desc, C::kIdesc, acc);
+              mma_i8_ss(d_tmem, make_smem_desc(a_smem + kk * 2 * 2048, 2048, 128, 0), b_desc, C::kIdesc, acc);
             }
           }
-          __syncwarp();
-        }
-        if (elect_one()) {
-          mma_commit(&x_empty[xs]);
-          if constexpr (C::kConvert) {
-            mma_commit(&a_empty[b]);
-          } else {
-            mma_commit(&w_empty[b]);
-          }
+          mma_commit(&kb_empty[xs]);
+          if constexpr (!C::kConvert) mma_commit(&w_empty[ws]);
         }
         __syncwarp();
         if (lane == 0 && it < 16) QQQ_STAMP(20 + it);
@@ -414,9 +414,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           xs = 0;
           xph ^= 1;
         }
-        if (++b == (C::kConvert ? (uint32_t)C::kABufs : (uint32_t)C::kWStages)) {
-          b = 0;
-          bph ^= 1;
+        if constexpr (!C::kConvert) {
+          if (++ws == C::kWStages) {
+            ws = 0;
+            wph ^= 1;
+          }
         }
       }
       if (elect_one()) mma_commit(&acc_full[j]);
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       while (si.next(tile, kb0, kb1)) {
 #pragma unroll 1
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          mbar_wait(&w_full[ws], wph);
+          conv_wait(&w_full[ws], wph);
           if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(4 + it);
           const uint32_t wst = wst0 + ws * C::kWBytes;
           uint4 v[kSlabs];
@@ -477,6 +479,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           uint32_t o[kSlabs][8];
 #pragma unroll
           for (int i = 0; i < kSlabs; ++i) {
+#ifdef QQQ_EXP_NO_CONV
+            o[i][0] = v[i].x; o[i][1] = v[i].y; o[i][2] = v[i].z; o[i][3] = v[i].w;
+            o[i][4] = v[i].x ^ s1[i]; o[i][5] = v[i].y; o[i][6] = v[i].z; o[i][7] = v[i].w;
+            continue;
+#endif
             if constexpr (MODE == kModePC) {
               pc_convert_word(v[i].x, o[i][0], o[i][4]);
               pc_convert_word(v[i].y, o[i][1], o[i][5]);
@@ -498,16 +505,20 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             ws = 0;
             wph ^= 1;
           }
-          mbar_wait(&a_empty[ab], aph ^ 1);
+          conv_wait(&kb_empty[ab], aph ^ 1);
           tc_fence_after();
           if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(64 + it);
           const uint32_t abase = a_lane + ab * C::kACols;
+#ifndef QQQ_EXP_NO_STTM
 #pragma unroll
           for (int i = 0; i < kSlabs; ++i) tmem_st8(abase + kPhases * i * 8, o[i]);
           tmem_wait_st();
+#else
+          if (o[0][0] == 0x12345678u && o[kSlabs - 1][7] == 0x9abcdef0u) tmem_st8(abase, o[0]);
+#endif
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&a_full[ab]);
+          if (lane == 0) mbar_arrive(&kb_full[ab]);
           if (++ab == C::kABufs) {
             ab = 0;
             aph ^= 1;
@@ -719,13 +730,17 @@ struct LaunchPlan {
   int64_t units;
 };
 
+// k-block depth per token tile: deep k-blocks amortise the per-k-block
+// handshakes of the decode tiles, short ones keep prefill activation stages small
+static constexpr int bk_for(int ntok) { return ntok <= 32 ? 512 : ntok <= 64 ? 256 : 128; }
+
 static LaunchPlan plan_for(int64_t M, int64_t N, int64_t K, int ntok, bool streamk, int force_grid) {
   LaunchPlan lp{};
   lp.ntok = ntok;
-  lp.bk = ntok <= 64 ? 256 : 128;
+  lp.bk = bk_for(ntok);
   lp.tok_tiles = (int)((M + ntok - 1) / ntok);
   lp.n_tiles = (int)(round_up(N, kTileN) / kTileN);
-  lp.kb_per_tile = (int)(round_up(K, kKPadTo) / lp.bk);
+  lp.kb_per_tile = (int)((round_up(K, kKPadTo) + lp.bk - 1) / lp.bk);  // last k-block may be partial
   lp.tiles = lp.n_tiles * lp.tok_tiles;
   lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
   const int sms = num_sms();
@@ -829,11 +844,11 @@ template <int MODE>
 static int launch_mode(int ntok, const CUtensorMap& map, const CUtensorMap& ymap, const GemmParams& p, int grid,
                        cudaStream_t st) {
   switch (ntok) {
-    case 16: return launch_t<MODE, 16, 256>(map, ymap, p, grid, st);
-    case 32: return launch_t<MODE, 32, 256>(map, ymap, p, grid, st);
-    case 64: return launch_t<MODE, 64, 256>(map, ymap, p, grid, st);
-    case 128: return launch_t<MODE, 128, 128>(map, ymap, p, grid, st);
-    case 256: return launch_t<MODE, 256, 128>(map, ymap, p, grid, st);
+    case 16: return launch_t<MODE, 16, bk_for(16)>(map, ymap, p, grid, st);
+    case 32: return launch_t<MODE, 32, bk_for(32)>(map, ymap, p, grid, st);
+    case 64: return launch_t<MODE, 64, bk_for(64)>(map, ymap, p, grid, st);
+    case 128: return launch_t<MODE, 128, bk_for(128)>(map, ymap, p, grid, st);
+    case 256: return launch_t<MODE, 256, bk_for(256)>(map, ymap, p, grid, st);
     default: return kErrConfig;
   }
 }

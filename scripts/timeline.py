@@ -15,6 +15,7 @@ for i in range(16):
     NAMES[20 + i] = f"mma{i}"
     NAMES[96 + i] = f"mma_xfull{i}"
     NAMES[112 + i] = f"mma_afull{i}"
+    NAMES[128 + i] = f"mma_issued{i}"
 for c in range(16):
     NAMES[44 + c] = f"epi0_c{c}"
     NAMES[64 + c] = f"conv_ae{c}"
@@ -37,7 +38,7 @@ aq = Q.quant_act_per_token(x)
 y = torch.empty((a.m, n), dtype=torch.float16, device=dev)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 for rep in range(3):
-    dbg = torch.zeros((1024, 128), dtype=torch.int64, device=dev)
+    dbg = torch.zeros((1024, 192), dtype=torch.int64, device=dev)
     cfg = dict(json.loads(a.cfg), dbg=dbg)
     flush.zero_()
     torch.cuda.synchronize()
