@@ -38,15 +38,6 @@
 
 namespace qqq {
 
-constexpr int kNumConvWarps = 16;  // 4 per TMEM lane quadrant
-constexpr int kConvWarp0 = 0;
-constexpr int kEpiWarp0 = kNumConvWarps, kNumEpiWarps = 8;  // two halves of 4 (one per TMEM lane quadrant)
-constexpr int kAllocWarp = kEpiWarp0 + kNumEpiWarps;
-constexpr int kActProducerWarp = kAllocWarp + 1;
-constexpr int kWProducerWarp = kAllocWarp + 2;
-constexpr int kMmaWarp = kAllocWarp + 3;
-constexpr int kNumThreads = (kMmaWarp + 1) * 32;
-constexpr int kSmemBudget = 225 * 1024;
 #ifdef QQQ_TIMELINE
 constexpr int kDbgSlots = 192;
 #endif
@@ -73,6 +64,28 @@ struct GemmParams {
 template <int MODE, int NTOK, int BK>
 struct Cfg {
   static constexpr bool kConvert = MODE != kModeI8;
+  // ---- CTA shape. Decode/mid tiles (NTOK <= 64) use a half-SM CTA: two per SM,
+  // so a CTA's prologue / first-byte latency / epilogue tail overlaps the other
+  // CTA's stream, and under PDL the next kernel's CTAs start (and prefetch
+  // their weights) in the slots this kernel's CTAs free. Prefill tiles use the
+  // whole SM (accumulators fill TMEM).
+  static constexpr bool kSmall = NTOK <= 64 && MODE != kModeI8;  // (I8 stages are 2x larger)
+  static constexpr int kCtasPerSm = kSmall ? 2 : 1;
+  static constexpr int kNumConvWarps = kSmall ? 8 : 16;  // 2 or 4 per TMEM lane quadrant
+  static constexpr int kNumEpiWarps = kSmall ? 4 : 8;    // 1 or 2 groups of 4 (one warp per lane quadrant)
+  static constexpr int kEpiGroups = kNumEpiWarps / 4;
+  static constexpr int kConvWarp0 = 0;
+  static constexpr int kEpiWarp0 = kNumConvWarps;
+  // big CTA: TMEM allocator, activation producer, weight producer and MMA warps;
+  // small CTA: one control warp (TMEM alloc + both producers + MMA issue)
+  static constexpr int kAllocWarp = kEpiWarp0 + kNumEpiWarps;
+  static constexpr int kActProducerWarp = kSmall ? -1 : kAllocWarp + 1;
+  static constexpr int kWProducerWarp = kSmall ? -1 : kAllocWarp + 2;
+  static constexpr int kMmaWarp = kSmall ? kAllocWarp : kAllocWarp + 3;
+  static constexpr int kNumThreads = (kMmaWarp + 1) * 32;
+  static constexpr int kSmemBudget = kSmall ? 111 * 1024 : 225 * 1024;
+  static constexpr int kTmemBudget = kSmall ? 256 : 512;
+  static constexpr int kEpiSmem = kEpiGroups * (2 * 4096 + 2 * 8192);  // y staging + split-K partial ring
   // Two rings. Weights: their own TMA ring (released by the converters once
   // the packed bytes are consumed, or by the MMA in I8 mode). K-blocks: ring
   // slot s = activation stage s = TMEM A buffer s, guarded by ONE full barrier
@@ -89,8 +102,8 @@ struct Cfg {
   static constexpr int kACols = BK / 4;
   static constexpr int kAccBufs = NTOK == 256 ? 1 : 2;
   static constexpr int kAccCols = kAccBufs * NTOK;
-  static constexpr int kABufsMax = kConvert ? (512 - kAccCols) / kACols : 8;
-  static constexpr int kRingBudget = kSmemBudget - 4096 - NTOK * 12 - 2 * 2 * 16 * 256 - 2 * 2 * 8192;
+  static constexpr int kABufsMax = kConvert ? (kTmemBudget - kAccCols) / kACols : 8;
+  static constexpr int kRingBudget = kSmemBudget - 2048 - NTOK * 12 - kEpiSmem;
   // k-block ring depth: what is left after 3 weight stages, at most 4 and at
   // most the number of TMEM A buffers that fit beside the accumulators
   static constexpr int kXStagesRaw = (kRingBudget - 3 * kWBytes) / kXBytes;
@@ -98,6 +111,7 @@ struct Cfg {
   static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > kXCap ? kXCap : kXStagesRaw);
   static constexpr int kABufs = kConvert ? kXStages : 0;
   static constexpr int kWStagesRaw = (kRingBudget - kXStages * kXBytes) / kWBytes;
+  static_assert(kXStages <= kABufsMax || !kConvert, "TMEM A buffers");
   static constexpr int kWStages = kWStagesRaw > 12 ? 12 : kWStagesRaw;
   static_assert(kWStages >= 2, "shared memory budget too small");
   static constexpr int kOffX = 0;  // 1024-aligned: NTOK*BK is a multiple of 2048
@@ -106,12 +120,13 @@ struct Cfg {
   static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 4 + 4;
   static constexpr int kOffSA = kOffBar + (kNumBars * 8 + 16 + 15) / 16 * 16;  // per-token scales of a tile (f64)
   static constexpr int kOffRS = kOffSA + NTOK * 8;                             // per-token code sums (int32)
-  static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;  // per epilogue half: 2 x [16 tok][128 ch] fp16
-  static constexpr int kOffPart = kOffY + 2 * 2 * 16 * 256;            // per half: 2 x 8 KiB split-K partial chunks
-  static constexpr int kSmemBytes = kOffPart + 2 * 2 * 8192 + 1024;     // +1024 alignment slack
-  static_assert(kSmemBytes <= 227 * 1024, "over the per-CTA shared memory limit");
+  static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;  // per epilogue group: 2 x [16 tok][128 ch] fp16
+  static constexpr int kOffPart = kOffY + kEpiGroups * 2 * 4096;       // per group: 2 x 8 KiB split-K partial chunks
+  static constexpr int kSmemBytes = kOffPart + kEpiGroups * 2 * 8192 + 1024;  // +1024 alignment slack
+  static_assert(kSmemBytes <= kSmemBudget + 1024 && kSmemBytes * kCtasPerSm <= 227 * 1024,
+                "over the per-CTA shared memory budget");
   static constexpr int kTmemNeed = kAccCols + kABufs * kACols;
-  static_assert(kTmemNeed <= 512, "TMEM over-subscribed");
+  static_assert(kTmemNeed <= kTmemBudget, "TMEM over-subscribed");
   static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
                                         : kTmemNeed <= 256 ? 256 : 512;
   // per-group: the converter emits w8 + 128 (no XOR); the MMA runs u8 x s8 and
@@ -269,7 +284,7 @@ QQQ_DEVICE int cta_of_unit(int64_t u, int64_t units, int grid) {
 // the kernel
 // ---------------------------------------------------------------------------
 template <int MODE, int NTOK, int BK>
-__global__ void __launch_bounds__(kNumThreads, 1)
+__global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NTOK, BK>::kCtasPerSm)
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap y_map,
                      const GemmParams p) {
   using C = Cfg<MODE, NTOK, BK>;
@@ -292,22 +307,22 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     QQQ_STAMP(0);
     griddep_launch_dependents();
     for (int s = 0; s < C::kXStages; ++s) {
-      mbar_init(&kb_full[s], C::kConvert ? kNumConvWarps + 1 : 1);
+      mbar_init(&kb_full[s], C::kConvert ? C::kNumConvWarps + 1 : 1);
       mbar_init(&kb_empty[s], 1);
     }
     for (int s = 0; s < C::kWStages; ++s) {
       mbar_init(&w_full[s], 1);
-      mbar_init(&w_empty[s], C::kConvert ? kNumConvWarps : 1);
+      mbar_init(&w_empty[s], C::kConvert ? C::kNumConvWarps : 1);
     }
     for (int j = 0; j < C::kAccBufs; ++j) {
       mbar_init(&acc_full[j], 1);
-      mbar_init(&acc_empty[j], kNumEpiWarps);
+      mbar_init(&acc_empty[j], C::kNumEpiWarps);
     }
     for (int i = 0; i < 4; ++i) mbar_init(&part_full[i], 1);
     mbar_fence_init();
   }
-  if (warp == kActProducerWarp && lane == 0) tma_prefetch_desc(&act_map);
-  if (warp == kAllocWarp) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == (C::kSmall ? C::kMmaWarp : C::kActProducerWarp) && lane == 0) tma_prefetch_desc(&act_map);
+  if (warp == C::kAllocWarp) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -318,7 +333,95 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   // then warp-uniform and live in uniform registers. Issuing tcgen05.mma from
   // a divergent single lane costs ~150 cycles per MMA (R2UR waterfall,
   // scripts/mma_probe.cu) against a 16-cycle issue floor at N = 16.
-  if (warp == kWProducerWarp) {
+  if (C::kSmall && warp == C::kMmaWarp) {
+    // ============ control warp (small CTA): producers + MMA issue ============
+    // One in-order loop over this CTA's k-blocks i = 0..total-1 (unit u0 + i):
+    //   weights run kWStages k-blocks ahead (prologue issued before the PDL
+    //   wait: they never depend on the previous kernel), activations kXStages
+    //   ahead; the weight stage of k-block i is refilled once k-block i is
+    //   converted (its kb_full completed), the activation slot of k-block i-1
+    //   once its MMAs retired.
+    SegIter si = make_iter(p);
+    const int64_t u0 = si.u;
+    const int total = (int)(si.u1 - si.u);
+    auto issue_w = [&](int i) {
+      const int64_t u = u0 + i;
+      const int tile = (int)(u / p.kb_per_tile), kb = (int)(u % p.kb_per_tile);
+      const int s = i % C::kWStages;
+      const int nss = min(BK / 128, p.ss_per_tile - kb * (BK / 128));
+      const uint32_t wbytes = (uint32_t)(nss * p.ss_bytes);
+      const int64_t ss0 = (int64_t)(tile / p.tok_tiles) * p.ss_per_tile + (int64_t)kb * (BK / 128);
+      mbar_arrive_expect_tx(&w_full[s], wbytes);
+      bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &w_full[s]);
+    };
+    auto issue_x = [&](int i) {
+      const int64_t u = u0 + i;
+      const int tile = (int)(u / p.kb_per_tile), kb = (int)(u % p.kb_per_tile);
+      const int s = i % C::kXStages;
+      mbar_arrive_expect_tx(&kb_full[s], C::kXBytes);
+      tma_load_3d(smem + C::kOffX + s * C::kXBytes, &act_map, 0, (tile % p.tok_tiles) * NTOK, kb * (BK / 128),
+                  &kb_full[s]);
+    };
+    if (elect_one()) {
+      for (int i = 0; i < C::kWStages && i < total; ++i) issue_w(i);
+    }
+    __syncwarp();
+    griddep_wait();  // the int8 activations come from the previous kernel
+    if (elect_one()) {
+      for (int i = 0; i < C::kXStages && i < total; ++i) issue_x(i);
+    }
+    __syncwarp();
+    int tile, kb0, kb1;
+    int i = 0;
+    uint32_t xs = 0, xph = 0, ws = 0, wph = 0, j = 0, jph = 0;
+    while (si.next(tile, kb0, kb1)) {
+      mbar_wait_sleep(&acc_empty[j], jph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + j * NTOK;
+#pragma unroll 1
+      for (int kb = kb0; kb < kb1; ++kb, ++i) {
+        mma_wait(&kb_full[xs], xph);  // activations landed and the A buffer is converted
+        tc_fence_after();
+        if (i + C::kWStages < total) {
+          mbar_wait(&w_empty[ws], wph);  // already complete: converters release it before kb_full
+          if (elect_one()) issue_w(i + C::kWStages);
+          __syncwarp();
+        }
+        const uint64_t b_desc0 = make_smem_desc(smem_u32(smem + C::kOffX + xs * C::kXBytes), 16, 1024, 2);
+        const uint32_t a_tmem = tmem_base + C::kAccCols + xs * C::kACols;
+        const uint32_t acc0 = kb > kb0 ? 1u : 0u;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 32; ++kk) {
+            const uint64_t b_desc = b_desc0 + (uint64_t)(((kk / 4) * (NTOK * 128) + (kk % 4) * 32) >> 4);
+            mma_i8_ts(d_tmem, a_tmem + kk * 8, b_desc, C::kIdesc, kk > 0 ? 1u : acc0);
+          }
+          mma_commit(&kb_empty[xs]);
+        }
+        __syncwarp();
+        // refill the activation slot of k-block i-1 (its MMAs have had a k-block to retire)
+        if (i >= 1 && i - 1 + C::kXStages < total) {
+          mbar_wait(&kb_empty[(i - 1) % C::kXStages], ((i - 1) / C::kXStages) & 1);
+          if (elect_one()) issue_x(i - 1 + C::kXStages);
+          __syncwarp();
+        }
+        if (++xs == C::kXStages) {
+          xs = 0;
+          xph ^= 1;
+        }
+        if (++ws == C::kWStages) {
+          ws = 0;
+          wph ^= 1;
+        }
+      }
+      if (elect_one()) mma_commit(&acc_full[j]);
+      __syncwarp();
+      if (++j == C::kAccBufs) {
+        j = 0;
+        jph ^= 1;
+      }
+    }
+  } else if (!C::kSmall && warp == C::kWProducerWarp) {
     // ===================== weight producer (bulk copies) =====================
     // Weights never depend on the previous kernel in the stream: no PDL wait,
     // so under PDL they stream in while the previous kernel drains.
@@ -348,7 +451,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       }
     }
     if (lane == 0) QQQ_STAMP(2);
-  } else if (warp == kActProducerWarp) {
+  } else if (!C::kSmall && warp == C::kActProducerWarp) {
     // ================== activation producer (3-D tensor TMA) ==================
     griddep_wait();  // the int8 activations come from the previous kernel
     if (lane == 0) QQQ_STAMP(3);
@@ -371,7 +474,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (!C::kSmall && warp == C::kMmaWarp) {
     // ============================ MMA issuer ============================
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
@@ -429,14 +532,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       }
       ++seg;
     }
-  } else if (warp >= kConvWarp0 && warp < kConvWarp0 + kNumConvWarps) {
+  } else if (warp >= C::kConvWarp0 && warp < C::kConvWarp0 + C::kNumConvWarps) {
     // ====================== INT4 -> INT8 converters ======================
     // Warp w owns TMEM lane quadrant q = w % 4 (rows 32q..32q+31) and every
     // other 32-k slab (parity w / 4): thread = one output channel.
     if constexpr (C::kConvert) {
       const int q = warp & 3, h = warp >> 2;  // quadrant, slab phase (0..kPhases-1)
       const int row = q * 32 + lane;
-      constexpr int kPhases = kNumConvWarps / 4;
+      constexpr int kPhases = C::kNumConvWarps / 4;
       constexpr int kSlabs = BK / 32 / kPhases;  // slabs per warp per k-block
       uint32_t magic;
       asm("mov.b32 %0, 0x64006400;" : "=r"(magic));  // a register operand for the fused and-or lop3
@@ -527,7 +630,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
       }
     }
-  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpiWarps) {
+  } else if (warp >= C::kEpiWarp0 && warp < C::kEpiWarp0 + C::kNumEpiWarps) {
     // ============================== epilogue ==============================
     // Whole tiles go straight from TMEM to y. A tile split over CTAs
     // b_first..b_last (stream-K) is finished by its OWNER b_first, for which it
@@ -540,14 +643,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     griddep_wait();  // y / acc / workspace / counters / s_a may belong to the previous kernel
     // two halves of 4 warps (each covering all 128 TMEM lanes) take alternate
     // 16-token chunks: half the per-thread work, same TMEM/partial/y protocol
-    const int eh = (warp - kEpiWarp0) >> 2;
+    constexpr int H = C::kEpiGroups;
+    const int eh = (warp - C::kEpiWarp0) >> 2;
     const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = q * 32 + lane;
-    const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..255
+    const int et = threadIdx.x - C::kEpiWarp0 * 32;  // 0..kAll-1
     const bool lead = et == 0;                    // segment-level lead (counters)
     const bool hlead = (et & 127) == 0;           // half lead (TMA stores, partial prefetch)
     const int kBarAll = 1, kBarHalf = 2 + eh;
-    constexpr int kAll = kNumEpiWarps * 32, kHalf = kAll / 2;
+    constexpr int kAll = C::kNumEpiWarps * 32, kHalf = kAll / H;
     double* sa_smem = reinterpret_cast<double*>(smem + C::kOffSA);
     int32_t* rs_smem = reinterpret_cast<int32_t*>(smem + C::kOffRS);
     uint8_t* ystage = smem + C::kOffY + eh * 8192;
@@ -590,12 +694,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       if (lead && seg < 4) QQQ_STAMP(36 + 2 * seg);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
       const int nchunks = (tvalid + 15) / 16;
-      const int nmine = (nchunks - eh + 1) / 2;  // chunks c = eh, eh + 2, ...
+      const int nmine = (nchunks - eh + H - 1) / H;  // chunks c = eh, eh + H, ...
       if (!owner) {
         // ---- contributor: red.add the partial into the tile's slot, release the counter
 #pragma unroll 1
         for (int li = 0; li < nmine; ++li) {
-          const int c0 = (eh + 2 * li) * 16;
+          const int c0 = (eh + H * li) * 16;
           uint32_t r[16];
           tmem_ld16(taddr + c0, r);
           tmem_wait_ld();
@@ -627,7 +731,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         auto part_issue = [&](int li) {
           const uint32_t pc = pchunk + li;
           mbar_arrive_expect_tx(&pfull[pc & 1], 8192);
-          bulk_g2s(pstage + (pc & 1) * 8192, slots + (int64_t)(eh + 2 * li) * 16 * 128, 8192, &pfull[pc & 1]);
+          bulk_g2s(pstage + (pc & 1) * 8192, slots + (int64_t)(eh + H * li) * 16 * 128, 8192, &pfull[pc & 1]);
         };
         if (!whole && hlead) {
           if (nmine > 0) part_issue(0);
@@ -635,7 +739,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
 #pragma unroll 1
         for (int li = 0; li < nmine; ++li) {
-          const int c0 = (eh + 2 * li) * 16;
+          const int c0 = (eh + H * li) * 16;
           uint32_t r[16];
           tmem_ld16(taddr + c0, r);
           tmem_wait_ld();
@@ -688,7 +792,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   }
 
   __syncthreads();
-  if (warp == kAllocWarp) {
+  if (warp == C::kAllocWarp) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);
   }
@@ -730,11 +834,13 @@ struct LaunchPlan {
   int64_t units;
 };
 
-// k-block depth per token tile: deep k-blocks amortise the per-k-block
-// handshakes of the decode tiles, short ones keep prefill activation stages small
-static constexpr int bk_for(int ntok) { return ntok <= 32 ? 512 : ntok <= 64 ? 256 : 128; }
+// k-block depth per token tile: 256 for the half-SM decode CTAs (8 converter
+// warps x 4 slabs, 64-column TMEM A buffers), 128 for prefill (small
+// activation stages beside 256-column accumulators)
+static constexpr int bk_for(int ntok) { return ntok <= 64 ? 256 : 128; }
+static constexpr int ctas_per_sm(int mode, int ntok) { return ntok <= 64 && mode != kModeI8 ? 2 : 1; }
 
-static LaunchPlan plan_for(int64_t M, int64_t N, int64_t K, int ntok, bool streamk, int force_grid) {
+static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, bool streamk, int force_grid) {
   LaunchPlan lp{};
   lp.ntok = ntok;
   lp.bk = bk_for(ntok);
@@ -743,12 +849,12 @@ static LaunchPlan plan_for(int64_t M, int64_t N, int64_t K, int ntok, bool strea
   lp.kb_per_tile = (int)((round_up(K, kKPadTo) + lp.bk - 1) / lp.bk);  // last k-block may be partial
   lp.tiles = lp.n_tiles * lp.tok_tiles;
   lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
-  const int sms = num_sms();
+  const int sms = num_sms() * ctas_per_sm(mode, ntok);  // CTA slots
   lp.max_segs = 1;
   if (streamk) {
     lp.aligned_tiles = 0;
     // Split tiles are finished by an owner CTA that waits for its contributors,
-    // so every CTA must be co-resident: never more CTAs than SMs (1 CTA/SM).
+    // so every CTA must be co-resident: never more CTAs than CTA slots.
     int g = force_grid > 0 ? std::min(force_grid, sms) : sms;
     lp.grid = (int)(lp.units < g ? lp.units : g);
     const int64_t per = lp.units / lp.grid;  // >= 1: most CTAs overlapping one tile
@@ -783,18 +889,19 @@ static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
   return T0 + ucta * u + fix + kE1 * (double)std::min<int64_t>(lp.ntok, M);
 }
 
-static LaunchPlan make_plan(int64_t M, int64_t N, int64_t K, int force_ntok, int force_grid, int force_split) {
+static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force_ntok, int force_grid,
+                            int force_split) {
   if (force_ntok > 0 || force_split >= 0 || force_grid > 0) {
     const int nt = force_ntok > 0 ? force_ntok : (M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256);
     const bool sk = force_split >= 0 ? force_split == 1 : nt <= 64;
-    return plan_for(M, N, K, nt, sk, force_grid);
+    return plan_for(mode, M, N, K, nt, sk, force_grid);
   }
   LaunchPlan best{};
   double best_t = 1e30;
   for (int nt : {16, 32, 64, 128, 256}) {
     if (nt > 16 && nt / 2 >= M) break;  // a smaller tile already covers every token
     for (int sk = 0; sk < 2; ++sk) {
-      const LaunchPlan lp = plan_for(M, N, K, nt, sk == 1, 0);
+      const LaunchPlan lp = plan_for(mode, M, N, K, nt, sk == 1, 0);
       if (lp.tiles > 65536) continue;
       const double t = plan_cost_us(lp, M);
       if (t < best_t) {
@@ -829,7 +936,7 @@ static int launch_t(const CUtensorMap& map, const CUtensorMap& ymap, const GemmP
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(grid);
-  lc.blockDim = dim3(kNumThreads);
+  lc.blockDim = dim3(C::kNumThreads);
   lc.dynamicSmemBytes = C::kSmemBytes;
   lc.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -861,7 +968,7 @@ extern "C" size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   size_t best = 0;  // any plan a caller may force or the cost model may pick
   for (int nt : {16, 32, 64, 128, 256}) {
-    LaunchPlan lp = plan_for(M, N, K, nt, true, 0);
+    LaunchPlan lp = plan_for(kModePG, M, N, K, nt, true, 0);  // slots do not change the slot bytes
     size_t b = plan_ws_bytes(lp);
     if (b > best) best = b;
   }
@@ -886,7 +993,7 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return kErrCuda;
 
-  LaunchPlan lp = make_plan(M, N, K, cfg ? cfg->ntok : 0, cfg ? cfg->grid : 0, cfg ? cfg->split : -1);
+  LaunchPlan lp = make_plan(mode, M, N, K, cfg ? cfg->ntok : 0, cfg ? cfg->grid : 0, cfg ? cfg->split : -1);
   if (lp.tiles > kMaxTiles) return kErrUnsupported;
   if (ws_bytes < plan_ws_bytes(lp)) return kErrConfig;
 
