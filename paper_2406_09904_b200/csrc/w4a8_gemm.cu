@@ -29,6 +29,7 @@
 //   * Epilogue: f64 (acc * s_a) * s_col then cvt.rn.f16.f64 -> bit-identical
 //     to the reference's f64 epilogue with a single final rounding.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -941,7 +942,8 @@ static int launch_t(const CUtensorMap& map, const CUtensorMap& ymap, const GemmP
   lc.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const int pdl = getenv("QQQ_NO_PDL") ? 0 : 1;  // developer A/B switch
+  attr[0].val.programmaticStreamSerializationAllowed = pdl;
   lc.attrs = attr;
   lc.numAttrs = 1;
   return cudaLaunchKernelEx(&lc, kern, map, ymap, p) == cudaSuccess ? kOk : kErrCuda;
