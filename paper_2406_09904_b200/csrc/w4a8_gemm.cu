@@ -711,9 +711,11 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[j]);
-        __threadfence();
+        // publish: CTA barrier, then ONE gpu-scope release by the lead (cumulative
+        // over the group's red.adds ordered before it by the barrier)
         named_bar_sync(kBarAll, kAll);
-        if (lead) atomicAdd(p.counters + tile, 1);
+        if (lead) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + tile) : "memory");
+        if (lead) QQQ_STAMP(61);
       } else {
         if (!whole) {
           // ---- owner of a split tile: wait for the other nsegs-1 contributions
@@ -724,6 +726,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
               asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
             } while (v < nsegs - 1);
             *cnt = 0;  // re-arm for the next launch (every contributor has arrived)
+            QQQ_STAMP(60);
           }
           named_bar_sync(kBarAll, kAll);
         }
@@ -748,6 +751,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
           if (!whole) {
             const uint32_t pc = pchunk + li;
             mbar_wait(&pfull[pc & 1], (pc >> 1) & 1);
+            if (lead && li == 0) QQQ_STAMP(62);
             const int32_t* part = reinterpret_cast<const int32_t*>(pstage + (pc & 1) * 8192);
 #pragma unroll
             for (int i = 0; i < 16; ++i) r[i] += (uint32_t)part[i * 128 + row];
@@ -789,7 +793,8 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
       if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
       ++seg;
     }
-    if (hlead) bulk_wait_all();  // y stores complete before the CTA retires
+    if (hlead) bulk_wait_read<0>();  // y stores have read their staging before the CTA retires
+    if (lead) QQQ_STAMP(63);
   }
 
   __syncthreads();

@@ -9,7 +9,8 @@ import bench as B
 import paper_2406_09904_b200 as Q
 from paper_2406_09904_b200 import gemm as G
 
-NAMES = {0: "start", 1: "setup", 2: "w_issued", 3: "dep_wait", 63: "end"}
+NAMES = {0: "start", 1: "setup", 2: "w_issued", 3: "dep_wait", 60: "own_cnt", 61: "contrib_done", 62: "part_ready",
+         63: "epi_end"}
 for i in range(16):
     NAMES[4 + i] = f"full{i}"
     NAMES[20 + i] = f"mma{i}"
