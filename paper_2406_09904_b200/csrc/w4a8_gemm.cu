@@ -78,12 +78,12 @@ struct Cfg {
   static constexpr int kConvWarp0 = 0;
   static constexpr int kEpiWarp0 = kNumConvWarps;
   // big CTA: TMEM allocator, activation producer, weight producer and MMA warps;
-  // small CTA: one control warp (TMEM alloc + both producers + MMA issue)
+  // small CTA: one producer warp for both rings, and the MMA warp allocates TMEM
   static constexpr int kAllocWarp = kEpiWarp0 + kNumEpiWarps;
-  static constexpr int kActProducerWarp = kSmall ? -1 : kAllocWarp + 1;
-  static constexpr int kWProducerWarp = kSmall ? -1 : kAllocWarp + 2;
+  static constexpr int kActProducerWarp = kSmall ? kAllocWarp + 1 : kAllocWarp + 1;
+  static constexpr int kWProducerWarp = kSmall ? kAllocWarp + 1 : kAllocWarp + 2;
   static constexpr int kMmaWarp = kSmall ? kAllocWarp : kAllocWarp + 3;
-  static constexpr int kNumThreads = (kMmaWarp + 1) * 32;
+  static constexpr int kNumThreads = ((kSmall ? kWProducerWarp : kMmaWarp) + 1) * 32;
   static constexpr int kSmemBudget = kSmall ? 111 * 1024 : 225 * 1024;
   static constexpr int kTmemBudget = kSmall ? 256 : 512;
   static constexpr int kEpiSmem = kEpiGroups * (2 * 4096 + 2 * 8192);  // y staging + split-K partial ring
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
     for (int i = 0; i < 4; ++i) mbar_init(&part_full[i], 1);
     mbar_fence_init();
   }
-  if (warp == (C::kSmall ? C::kMmaWarp : C::kActProducerWarp) && lane == 0) tma_prefetch_desc(&act_map);
+  if (warp == C::kActProducerWarp && lane == 0) tma_prefetch_desc(&act_map);
   if (warp == C::kAllocWarp) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
@@ -334,95 +334,78 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
   // then warp-uniform and live in uniform registers. Issuing tcgen05.mma from
   // a divergent single lane costs ~150 cycles per MMA (R2UR waterfall,
   // scripts/mma_probe.cu) against a 16-cycle issue floor at N = 16.
-  if (C::kSmall && warp == C::kMmaWarp) {
-    // ============ control warp (small CTA): producers + MMA issue ============
-    // One in-order loop over this CTA's k-blocks i = 0..total-1 (unit u0 + i):
-    //   weights run kWStages k-blocks ahead (prologue issued before the PDL
-    //   wait: they never depend on the previous kernel), activations kXStages
-    //   ahead; the weight stage of k-block i is refilled once k-block i is
-    //   converted (its kb_full completed), the activation slot of k-block i-1
-    //   once its MMAs retired.
+  if (C::kSmall && warp == C::kWProducerWarp) {
+    // ========== producer warp (small CTA): weight + activation rings ==========
+    // One in-order loop over this CTA's k-blocks i = 0..total-1: the weight
+    // stage of k-block i is refilled (k-block i + kWStages) once the
+    // converters released it, the activation slot of k-block i once its MMAs
+    // retired. The weight prologue is issued before the PDL wait (weights
+    // never depend on the previous kernel).
     SegIter si = make_iter(p);
-    const int64_t u0 = si.u;
     const int total = (int)(si.u1 - si.u);
-    auto issue_w = [&](int i) {
-      const int64_t u = u0 + i;
-      const int tile = (int)(u / p.kb_per_tile), kb = (int)(u % p.kb_per_tile);
-      const int s = i % C::kWStages;
-      const int nss = min(BK / 128, p.ss_per_tile - kb * (BK / 128));
-      const uint32_t wbytes = (uint32_t)(nss * p.ss_bytes);
-      const int64_t ss0 = (int64_t)(tile / p.tok_tiles) * p.ss_per_tile + (int64_t)kb * (BK / 128);
-      mbar_arrive_expect_tx(&w_full[s], wbytes);
-      bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &w_full[s]);
+    // incremental (n_tile, token tile, k-block) cursors: no division in the loop
+    struct Cur {
+      int n_tile, tt, kb;
     };
-    auto issue_x = [&](int i) {
-      const int64_t u = u0 + i;
-      const int tile = (int)(u / p.kb_per_tile), kb = (int)(u % p.kb_per_tile);
-      const int s = i % C::kXStages;
-      mbar_arrive_expect_tx(&kb_full[s], C::kXBytes);
-      tma_load_3d(smem + C::kOffX + s * C::kXBytes, &act_map, 0, (tile % p.tok_tiles) * NTOK, kb * (BK / 128),
-                  &kb_full[s]);
-    };
-    if (elect_one()) {
-      for (int i = 0; i < C::kWStages && i < total; ++i) issue_w(i);
-    }
-    __syncwarp();
-    griddep_wait();  // the int8 activations come from the previous kernel
-    if (elect_one()) {
-      for (int i = 0; i < C::kXStages && i < total; ++i) issue_x(i);
-    }
-    __syncwarp();
-    int tile, kb0, kb1;
-    int i = 0;
-    uint32_t xs = 0, xph = 0, ws = 0, wph = 0, j = 0, jph = 0;
-    while (si.next(tile, kb0, kb1)) {
-      mbar_wait_sleep(&acc_empty[j], jph ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + j * NTOK;
-#pragma unroll 1
-      for (int kb = kb0; kb < kb1; ++kb, ++i) {
-        mma_wait(&kb_full[xs], xph);  // activations landed and the A buffer is converted
-        tc_fence_after();
-        if (i + C::kWStages < total) {
-          mbar_wait(&w_empty[ws], wph);  // already complete: converters release it before kb_full
-          if (elect_one()) issue_w(i + C::kWStages);
-          __syncwarp();
-        }
-        const uint64_t b_desc0 = make_smem_desc(smem_u32(smem + C::kOffX + xs * C::kXBytes), 16, 1024, 2);
-        const uint32_t a_tmem = tmem_base + C::kAccCols + xs * C::kACols;
-        const uint32_t acc0 = kb > kb0 ? 1u : 0u;
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < BK / 32; ++kk) {
-            const uint64_t b_desc = b_desc0 + (uint64_t)(((kk / 4) * (NTOK * 128) + (kk % 4) * 32) >> 4);
-            mma_i8_ts(d_tmem, a_tmem + kk * 8, b_desc, C::kIdesc, kk > 0 ? 1u : acc0);
-          }
-          mma_commit(&kb_empty[xs]);
-        }
-        __syncwarp();
-        // refill the activation slot of k-block i-1 (its MMAs have had a k-block to retire)
-        if (i >= 1 && i - 1 + C::kXStages < total) {
-          mbar_wait(&kb_empty[(i - 1) % C::kXStages], ((i - 1) / C::kXStages) & 1);
-          if (elect_one()) issue_x(i - 1 + C::kXStages);
-          __syncwarp();
-        }
-        if (++xs == C::kXStages) {
-          xs = 0;
-          xph ^= 1;
-        }
-        if (++ws == C::kWStages) {
-          ws = 0;
-          wph ^= 1;
+    auto adv = [&](Cur& c) {
+      if (++c.kb == p.kb_per_tile) {
+        c.kb = 0;
+        if (++c.tt == p.tok_tiles) {
+          c.tt = 0;
+          ++c.n_tile;
         }
       }
-      if (elect_one()) mma_commit(&acc_full[j]);
+    };
+    const int tile0 = (int)(si.u / p.kb_per_tile);
+    Cur wc{tile0 / p.tok_tiles, tile0 % p.tok_tiles, (int)(si.u % p.kb_per_tile)};
+    Cur xc = wc;
+    uint32_t wi = 0, xi = 0;  // ring slots of the next copies
+    auto issue_w = [&]() {
+      if (elect_one()) {
+        const int nss = min(BK / 128, p.ss_per_tile - wc.kb * (BK / 128));
+        const uint32_t wbytes = (uint32_t)(nss * p.ss_bytes);
+        const int64_t ss0 = (int64_t)wc.n_tile * p.ss_per_tile + (int64_t)wc.kb * (BK / 128);
+        mbar_arrive_expect_tx(&w_full[wi], wbytes);
+        bulk_g2s(smem + C::kOffW + wi * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &w_full[wi]);
+      }
       __syncwarp();
-      if (++j == C::kAccBufs) {
-        j = 0;
-        jph ^= 1;
+      adv(wc);
+      if (++wi == C::kWStages) wi = 0;
+    };
+    auto issue_x = [&]() {
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&kb_full[xi], C::kXBytes);
+        tma_load_3d(smem + C::kOffX + xi * C::kXBytes, &act_map, 0, xc.tt * NTOK, xc.kb * (BK / 128), &kb_full[xi]);
+      }
+      __syncwarp();
+      adv(xc);
+      if (++xi == C::kXStages) xi = 0;
+    };
+    for (int i = 0; i < C::kWStages && i < total; ++i) issue_w();
+    griddep_wait();  // the int8 activations come from the previous kernel
+    for (int i = 0; i < C::kXStages && i < total; ++i) issue_x();
+    uint32_t ws = 0, wph = 0, xs = 0, xph = 0;
+#pragma unroll 1
+    for (int i = 0; i < total; ++i) {
+      if (i + C::kWStages < total) {
+        mbar_wait_sleep(&w_empty[ws], wph);
+        issue_w();
+      }
+      if (++ws == C::kWStages) {
+        ws = 0;
+        wph ^= 1;
+      }
+      if (i + C::kXStages < total) {
+        mbar_wait_sleep(&kb_empty[xs], xph);
+        issue_x();
+        if (lane == 0 && i < 16) QQQ_STAMP(112 + i);
+      }
+      if (++xs == C::kXStages) {
+        xs = 0;
+        xph ^= 1;
       }
     }
-  } else if (!C::kSmall && warp == C::kWProducerWarp) {
+  } else if (!C::kSmall && warp == C::kWProducerWarp) {  // big CTA
     // ===================== weight producer (bulk copies) =====================
     // Weights never depend on the previous kernel in the stream: no PDL wait,
     // so under PDL they stream in while the previous kernel drains.
@@ -475,7 +458,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
         }
       }
     }
-  } else if (!C::kSmall && warp == C::kMmaWarp) {
+  } else if (warp == C::kMmaWarp) {
     // ============================ MMA issuer ============================
     SegIter si = make_iter(p);
     int tile, kb0, kb1;

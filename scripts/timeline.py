@@ -15,7 +15,7 @@ for i in range(16):
     NAMES[4 + i] = f"full{i}"
     NAMES[20 + i] = f"mma{i}"
     NAMES[96 + i] = f"mma_xfull{i}"
-    NAMES[112 + i] = f"mma_afull{i}"
+    NAMES[112 + i] = f"ctl_xissued{i}"
     NAMES[128 + i] = f"mma_issued{i}"
 for c in range(16):
     NAMES[44 + c] = f"epi0_c{c}"
