@@ -86,7 +86,7 @@ struct Cfg {
   static constexpr int kNumThreads = ((kSmall ? kWProducerWarp : kMmaWarp) + 1) * 32;
   static constexpr int kSmemBudget = kSmall ? 111 * 1024 : 225 * 1024;
   static constexpr int kTmemBudget = kSmall ? 256 : 512;
-  static constexpr int kEpiSmem = kEpiGroups * (2 * 4096 + 2 * 8192);  // y staging + split-K partial ring
+  static constexpr int kEpiSmem = kNumEpiWarps * 2048 + kEpiGroups * 2 * 8192;  // y staging + split-K partial ring
   // Two rings. Weights: their own TMA ring (released by the converters once
   // the packed bytes are consumed, or by the MMA in I8 mode). K-blocks: ring
   // slot s = activation stage s = TMEM A buffer s, guarded by ONE full barrier
@@ -121,8 +121,8 @@ struct Cfg {
   static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 4 + 4;
   static constexpr int kOffSA = kOffBar + (kNumBars * 8 + 16 + 15) / 16 * 16;  // per-token scales of a tile (f64)
   static constexpr int kOffRS = kOffSA + NTOK * 8;                             // per-token code sums (int32)
-  static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;  // per epilogue group: 2 x [16 tok][128 ch] fp16
-  static constexpr int kOffPart = kOffY + kEpiGroups * 2 * 4096;       // per group: 2 x 8 KiB split-K partial chunks
+  static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;  // per epilogue warp: 2 x [16 tok][32 ch] fp16
+  static constexpr int kOffPart = kOffY + kNumEpiWarps * 2048;         // per group: 2 x 8 KiB split-K partial chunks
   static constexpr int kSmemBytes = kOffPart + kEpiGroups * 2 * 8192 + 1024;  // +1024 alignment slack
   static_assert(kSmemBytes <= kSmemBudget + 1024 && kSmemBytes * kCtasPerSm <= 227 * 1024,
                 "over the per-CTA shared memory budget");
@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
     constexpr int kAll = C::kNumEpiWarps * 32, kHalf = kAll / H;
     double* sa_smem = reinterpret_cast<double*>(smem + C::kOffSA);
     int32_t* rs_smem = reinterpret_cast<int32_t*>(smem + C::kOffRS);
-    uint8_t* ystage = smem + C::kOffY + eh * 8192;
+    uint8_t* ystage = smem + C::kOffY + (warp - C::kEpiWarp0) * 2048;  // per warp: 2 x [16 tok][32 ch] fp16
     uint8_t* pstage = smem + C::kOffPart + eh * 16384;
     uint64_t* pfull = part_full + 2 * eh;
     uint32_t ych = 0;     // y staging chunks issued by this half
@@ -751,18 +751,19 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
           }
           store_outputs(p, r, sa_smem + c0, tok0 + c0, tvalid - c0, n, n_ok, s_col);
           if (p.y_tma) {
-            // y chunk -> staging [16 tok][128 ch] fp16 -> one TMA store (OOB rows/cols clipped)
-            uint16_t* stg = reinterpret_cast<uint16_t*>(ystage + (ych & 1) * 4096);
-            if (hlead) bulk_wait_read<1>();  // the store that used this buffer two chunks ago has read it
-            named_bar_sync(kBarHalf, kHalf);
+            // y chunk -> this warp's staging [16 tok][32 ch] fp16 -> its own TMA store
+            // (OOB rows/cols clipped): no cross-warp barrier on the store path
+            uint16_t* stg = reinterpret_cast<uint16_t*>(ystage) + (ych & 1) * 512;
             uint16_t h[16];
             dequant16(r, sa_smem + c0, s_col, h);
+            if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer two chunks ago has read it
+            __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) stg[i * 128 + row] = h[i];
+            for (int i = 0; i < 16; ++i) stg[i * 32 + lane] = h[i];
             fence_proxy_async_smem();
-            named_bar_sync(kBarHalf, kHalf);
-            if (hlead) {
-              tma_store_2d(&y_map, stg, n_tile * 128, tok0 + c0);
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&y_map, stg, n_tile * 128 + q * 32, tok0 + c0);
               bulk_commit();
             }
             ++ych;
@@ -776,7 +777,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
       if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
       ++seg;
     }
-    if (hlead) bulk_wait_read<0>();  // y stores have read their staging before the CTA retires
+    if (lane == 0) bulk_wait_read<0>();  // y stores have read their staging before the CTA retires
     if (lead) QQQ_STAMP(63);
   }
 
@@ -1005,7 +1006,7 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   if (s_col && y && (ldy * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
     cuuint64_t ydims[2] = {(cuuint64_t)N, (cuuint64_t)M};
     cuuint64_t ystr[1] = {(cuuint64_t)(ldy * 2)};
-    cuuint32_t ybox[2] = {128u, 16u};
+    cuuint32_t ybox[2] = {32u, 16u};  // one epilogue warp's [16 tok][32 ch] chunk
     cuuint32_t yes[2] = {1u, 1u};
     if (enc(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, y, ydims, ystr, ybox, yes, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
