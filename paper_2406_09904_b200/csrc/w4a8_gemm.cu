@@ -72,8 +72,14 @@ struct Cfg {
   // whole SM (accumulators fill TMEM).
   static constexpr bool kSmall = NTOK <= 64 && MODE != kModeI8;  // (I8 stages are 2x larger)
   static constexpr int kCtasPerSm = kSmall ? 2 : 1;
-  static constexpr int kNumConvWarps = kSmall ? 8 : 16;  // 2 or 4 per TMEM lane quadrant
-  static constexpr int kNumEpiWarps = kSmall ? 4 : 8;    // 1 or 2 groups of 4 (one warp per lane quadrant)
+#ifndef QQQ_BIG_CONV_WARPS
+#define QQQ_BIG_CONV_WARPS 8
+#endif
+  // 2 per TMEM lane quadrant: each converter warp handles >= 2 slabs per
+  // k-block so the per-k-block handshake cost (~80 instructions per warp) stays
+  // well below the conversion work
+  static constexpr int kNumConvWarps = kSmall ? 8 : QQQ_BIG_CONV_WARPS;
+  static constexpr int kNumEpiWarps = kSmall ? 4 : 8;  // 1 or 2 groups of 4 (one warp per lane quadrant)
   static constexpr int kEpiGroups = kNumEpiWarps / 4;
   static constexpr int kConvWarp0 = 0;
   static constexpr int kEpiWarp0 = kNumConvWarps;
@@ -448,7 +454,11 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait_sleep(&kb_empty[s], ph ^ 1);
         if (elect_one()) {
+#ifdef QQQ_EXP_HALF_X
+          mbar_arrive_expect_tx(&kb_full[s], NTOK >= 128 ? C::kXBytes / 2 : C::kXBytes);
+#else
           mbar_arrive_expect_tx(&kb_full[s], C::kXBytes);
+#endif
           tma_load_3d(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0, kb * (BK / 128), &kb_full[s]);
         }
         __syncwarp();
@@ -992,7 +1002,11 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   const int64_t katoms = (K + 127) / 128;
   cuuint64_t dims[3] = {128u, (cuuint64_t)M, (cuuint64_t)katoms};
   cuuint64_t strides[2] = {(cuuint64_t)ldq, 128u};
+#ifdef QQQ_EXP_HALF_X
+  cuuint32_t box[3] = {128u, (cuuint32_t)(lp.ntok >= 128 ? lp.ntok / 2 : lp.ntok), (cuuint32_t)(lp.bk / 128)};
+#else
   cuuint32_t box[3] = {128u, (cuuint32_t)lp.ntok, (cuuint32_t)(lp.bk / 128)};
+#endif
   cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)aq, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
