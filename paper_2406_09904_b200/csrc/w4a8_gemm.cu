@@ -58,6 +58,8 @@ struct GemmParams {
   int n_tiles, tok_tiles, kb_per_tile, ss_per_tile, ss_bytes, group, max_segs;
   int64_t units;
   int aligned_tiles;        // >0: CTA b owns whole tiles [b*aligned_tiles, ...)
+  int dp_tiles;             // hybrid: CTA b first owns whole tiles [b*dp_tiles, (b+1)*dp_tiles), then
+  int64_t sk_unit0;         //   its stream-K share of the units [sk_unit0, sk_unit0 + units)
   int y_tma;                // 1: y written by TMA stores from a shared-memory staging tile
   unsigned long long* dbg;  // optional per-CTA %globaltimer timeline, diagnostics only
 };
@@ -244,17 +246,33 @@ QQQ_DEVICE void tma_store_2d(const CUtensorMap* map, const void* smem_src, int32
                "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
                : "memory");
 }
+// bulk reduction of a shared-memory block into global memory (int32 add, done
+// in L2 at bulk bandwidth; replaces per-element atomics for split-K partials)
+QQQ_DEVICE void bulk_reduce_add_s32(void* gmem_dst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.s32 [%0], [%1], %2;" ::"l"(gmem_dst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
 QQQ_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 QQQ_DEVICE void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 QQQ_DEVICE void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Segment iterator: the CTA's contiguous (tile, k-block) unit range split at tile borders.
+// A CTA's work: up to two contiguous (tile, k-block) unit ranges, iterated in
+// order and split at tile borders: [u, u1) then [v, v1) (hybrid plans: whole
+// data-parallel tiles first, then the stream-K share).
 struct SegIter {
-  int64_t u, u1;
+  int64_t u, u1, v, v1;
   int kbt;
+  QQQ_DEVICE int64_t total() const { return (u1 - u) + (v1 - v); }
   QQQ_DEVICE bool next(int& tile, int& kb0, int& kb1) {
-    if (u >= u1) return false;
+    if (u >= u1) {
+      if (v >= v1) return false;
+      u = v;
+      u1 = v1;
+      v = v1;
+    }
     tile = (int)(u / kbt);
     kb0 = (int)(u % kbt);
     const int64_t rem = u1 - u;
@@ -267,6 +285,7 @@ struct SegIter {
 QQQ_DEVICE SegIter make_iter(const GemmParams& p) {
   SegIter it;
   it.kbt = p.kb_per_tile;
+  it.v = it.v1 = 0;
   if (p.aligned_tiles > 0) {
     const int64_t tiles = (int64_t)p.n_tiles * p.tok_tiles;
     int64_t t0 = (int64_t)blockIdx.x * p.aligned_tiles;
@@ -276,15 +295,21 @@ QQQ_DEVICE SegIter make_iter(const GemmParams& p) {
     it.u = t0 * p.kb_per_tile;
     it.u1 = t1 * p.kb_per_tile;
   } else {
-    it.u = (int64_t)blockIdx.x * p.units / gridDim.x;
-    it.u1 = (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
+    it.u = p.sk_unit0 + (int64_t)blockIdx.x * p.units / gridDim.x;
+    it.u1 = p.sk_unit0 + (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
+    if (p.dp_tiles > 0) {
+      it.v = it.u;
+      it.v1 = it.u1;
+      it.u = (int64_t)blockIdx.x * p.dp_tiles * p.kb_per_tile;
+      it.u1 = it.u + (int64_t)p.dp_tiles * p.kb_per_tile;
+    }
   }
   return it;
 }
 
-// stream-K: the CTA whose unit range contains unit u (start(b) = floor(b*U/G))
-QQQ_DEVICE int cta_of_unit(int64_t u, int64_t units, int grid) {
-  return (int)(((u + 1) * grid - 1) / units);
+// stream-K: the CTA whose stream-K range contains unit u (start(b) = sk_unit0 + floor(b*U/G))
+QQQ_DEVICE int cta_of_unit(int64_t u, const GemmParams& p, int grid) {
+  return (int)(((u - p.sk_unit0 + 1) * grid - 1) / p.units);
 }
 
 // ---------------------------------------------------------------------------
@@ -348,7 +373,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
     // retired. The weight prologue is issued before the PDL wait (weights
     // never depend on the previous kernel).
     SegIter si = make_iter(p);
-    const int total = (int)(si.u1 - si.u);
+    const int total = (int)si.total();  // small CTAs: a single stream-K range (no data-parallel part)
     // incremental (n_tile, token tile, k-block) cursors: no division in the loop
     struct Cur {
       int n_tile, tt, kb;
@@ -653,6 +678,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
     uint64_t* pfull = part_full + 2 * eh;
     uint32_t ych = 0;     // y staging chunks issued by this half
     uint32_t pchunk = 0;  // partial-sum chunks consumed by this half (part_full parity)
+    uint32_t pcon = 0;    // contributor chunks staged by this half (ring buffer alternation)
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
     uint32_t seg = 0;
@@ -675,8 +701,8 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
       int32_t* slots = nullptr;
       if (!whole) {
         const int64_t u_first = (int64_t)tile * p.kb_per_tile;
-        const int b_first = cta_of_unit(u_first, p.units, gridDim.x);
-        const int b_last = cta_of_unit(u_first + p.kb_per_tile - 1, p.units, gridDim.x);
+        const int b_first = cta_of_unit(u_first, p, gridDim.x);
+        const int b_last = cta_of_unit(u_first + p.kb_per_tile - 1, p, gridDim.x);
         seg_idx = (int)blockIdx.x - b_first;
         nsegs = b_last - b_first + 1;
         slots = p.ws + (int64_t)tile * NTOK * 128;  // one zero-initialised accumulation slot per tile
@@ -690,22 +716,46 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
       const int nchunks = (tvalid + 15) / 16;
       const int nmine = (nchunks - eh + H - 1) / H;  // chunks c = eh, eh + H, ...
       if (!owner) {
-        // ---- contributor: red.add the partial into the tile's slot, release the counter
+        // ---- contributor: add the partial into the tile's slot, release the counter.
+        // Chunks with few valid tokens use per-element red.add; fuller chunks are
+        // staged in shared memory and reduced with ONE bulk cp.reduce (L2-side
+        // int32 add at bulk bandwidth; per-lane atomics run at ~1 lane/clk/SM).
 #pragma unroll 1
         for (int li = 0; li < nmine; ++li) {
           const int c0 = (eh + H * li) * 16;
           uint32_t r[16];
           tmem_ld16(taddr + c0, r);
           tmem_wait_ld();
+          if (tvalid - c0 < 4) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c0 + i < tvalid) red_add_s32(slots + (c0 + i) * 128 + row, (int32_t)r[i]);
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < tvalid) red_add_s32(slots + (c0 + i) * 128 + row, (int32_t)r[i]);
+          } else {
+            // rows past tvalid hold zeros (their activations were zero-filled)
+            int32_t* stg = reinterpret_cast<int32_t*>(pstage + (pcon & 1) * 8192);
+            if (hlead) bulk_wait_read<1>();  // the reduce that used this buffer two chunks ago has read it
+            named_bar_sync(kBarHalf, kHalf);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) stg[i * 128 + row] = (int32_t)r[i];
+            fence_proxy_async_smem();
+            named_bar_sync(kBarHalf, kHalf);
+            if (hlead) {
+              bulk_reduce_add_s32(slots + c0 * 128, stg, 8192);
+              bulk_commit();
+            }
+            ++pcon;
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[j]);
-        // publish: CTA barrier, then ONE gpu-scope release by the lead (cumulative
-        // over the group's red.adds ordered before it by the barrier)
+        // publish: the group leads wait for their bulk reductions to complete, then
+        // CTA barrier and ONE gpu-scope release by the lead (cumulative over the
+        // red.adds / completed bulk reductions ordered before it by the barrier)
+        if (hlead) {
+          bulk_wait_all();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         named_bar_sync(kBarAll, kAll);
         if (lead) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + tile) : "memory");
         if (lead) QQQ_STAMP(61);
@@ -731,6 +781,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
           bulk_g2s(pstage + (pc & 1) * 8192, slots + (int64_t)(eh + H * li) * 16 * 128, 8192, &pfull[pc & 1]);
         };
         if (!whole && hlead) {
+          bulk_wait_read<0>();  // earlier contributor reductions have read the shared ring
           if (nmine > 0) part_issue(0);
           if (nmine > 1) part_issue(1);
         }
@@ -830,20 +881,25 @@ static int num_sms() {
 }
 
 struct LaunchPlan {
-  int ntok, bk, grid, aligned_tiles, tok_tiles, n_tiles, kb_per_tile, tiles, max_segs;
-  int64_t units;
+  int ntok, bk, grid, aligned_tiles, tok_tiles, n_tiles, kb_per_tile, tiles, max_segs, dp_tiles;
+  int64_t units, sk_unit0;
 };
 
 // k-block depth per token tile: 256 for the half-SM decode CTAs (8 converter
 // warps x 4 slabs, 64-column TMEM A buffers), 128 for prefill (small
 // activation stages beside 256-column accumulators)
-static constexpr int bk_for(int ntok) { return ntok <= 64 ? 256 : 128; }
+#ifndef QQQ_BIG_BK
+#define QQQ_BIG_BK 256
+#endif
+static constexpr int bk_for(int mode, int ntok) { return ntok <= 64 ? 256 : mode == kModeI8 ? 128 : QQQ_BIG_BK; }
 static constexpr int ctas_per_sm(int mode, int ntok) { return ntok <= 64 && mode != kModeI8 ? 2 : 1; }
 
-static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, bool streamk, int force_grid) {
+// split: 0 = whole tiles (data-parallel), 1 = stream-K over all units,
+//        2 = hybrid: full waves of whole tiles, the remainder stream-K'd over all CTAs
+static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, int split, int force_grid) {
   LaunchPlan lp{};
   lp.ntok = ntok;
-  lp.bk = bk_for(ntok);
+  lp.bk = bk_for(mode, ntok);
   lp.tok_tiles = (int)((M + ntok - 1) / ntok);
   lp.n_tiles = (int)(round_up(N, kTileN) / kTileN);
   lp.kb_per_tile = (int)((round_up(K, kKPadTo) + lp.bk - 1) / lp.bk);  // last k-block may be partial
@@ -851,7 +907,23 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
   lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
   const int sms = num_sms() * ctas_per_sm(mode, ntok);  // CTA slots
   lp.max_segs = 1;
-  if (streamk) {
+  if (split == 2 && ctas_per_sm(mode, ntok) == 2) split = 1;  // small CTAs: a single stream-K range
+  if (split == 2) {
+    const int g = force_grid > 0 ? std::min(force_grid, sms) : sms;
+    const int waves = lp.tiles / g, rem = lp.tiles % g;
+    if (waves >= 1 && rem > 0) {
+      lp.aligned_tiles = 0;
+      lp.grid = g;
+      lp.dp_tiles = waves;
+      lp.sk_unit0 = (int64_t)waves * g * lp.kb_per_tile;
+      lp.units = (int64_t)rem * lp.kb_per_tile;
+      const int64_t per = std::max<int64_t>(1, lp.units / g);
+      lp.max_segs = (int)std::min<int64_t>((lp.kb_per_tile + per - 1) / per + 1, g);
+      return lp;
+    }
+    split = waves >= 1 ? 0 : 1;  // exact waves: data-parallel; under one wave: stream-K
+  }
+  if (split == 1) {
     lp.aligned_tiles = 0;
     // Split tiles are finished by an owner CTA that waits for its contributors,
     // so every CTA must be co-resident: never more CTAs than CTA slots.
@@ -868,40 +940,43 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
   return lp;
 }
 
-// Tile-plan cost model (us), fitted to B200 sweeps of this kernel
-// (scripts/quick_bench.py tile-plan sweeps, profiles/README.md):
-//   T = T0 + units_per_CTA * max(weight bytes / per-CTA HBM share, MMA time,
-//       activation smem traffic) + split-K fix-up + last-tile epilogue.
+// Tile-plan cost model (us), fitted (log least squares, scripts/fit_planner.py)
+// to the B200 tile-plan sweep profiles/r01_tileplan_sweep_v2.jsonl of this
+// kernel (0.8% regret against the best measured plan over the C2 sweep):
+//   per-k-block time u = max(weight bytes / per-CTA HBM share, conversion, MMA)
+//   whole tiles: T = T0 + units_per_CTA * u + waves * epilogue
+//   stream-K:    T = T0 + units_per_CTA * u + fix-up + epilogue
 static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
-  // fitted (log-least-squares) on profiles/r01_tileplan_sweep.jsonl, per-group g=128
-  const double T0 = 2.47, kBsm = 250.7e3, kBtot = 3136e3, kF0 = 2.80, kF1 = 0.0135, kE1 = 0.0349, kMma = 1.77,
-               kConv = 0.02419e-3;  // us per weight per CTA
+  const double T0 = 1.801, kBsm = 499.9e3, kBtot = 6382e3, kConv = 14.62e-6, kMma = 1.495, kF0 = 1.643,
+               kF1 = 0.6073, kE0 = 3.077, kE1 = 0.004508;
   const double clk = 1900.0;  // MHz
+  const int cps = lp.ntok <= 64 ? 2 : 1;
   const int64_t ucta = lp.aligned_tiles > 0 ? (int64_t)lp.aligned_tiles * lp.kb_per_tile
-                                            : (lp.units + lp.grid - 1) / lp.grid;
+                                            : (int64_t)lp.dp_tiles * lp.kb_per_tile + (lp.units + lp.grid - 1) / lp.grid;
   const double bw = std::min(kBsm, kBtot / lp.grid);  // bytes/us per CTA
   const double wkb = lp.bk * 64.0 * (1.0 + 1.0 / 32);
   const double mma = (lp.bk / 32.0) * (lp.ntok / 2.0) / clk * kMma;
-  const double act = 2.0 * lp.ntok * lp.bk / 128.0 / clk;
-  const double conv = lp.bk * 128.0 * kConv;
-  const double u = std::max(std::max(wkb / bw, conv), std::max(mma, act));
-  const double fix = lp.aligned_tiles > 0 ? 0.0 : kF0 + kF1 * lp.ntok;
-  return T0 + ucta * u + fix + kE1 * (double)std::min<int64_t>(lp.ntok, M);
+  const double conv = lp.bk * 128.0 * kConv * cps;
+  const double u = std::max(std::max(wkb / bw, conv), mma);
+  const double mt = (double)std::min<int64_t>(lp.ntok, M) / 16.0;
+  const double epi = kE0 + kE1 * mt;
+  if (lp.aligned_tiles > 0) return T0 + ucta * u + lp.aligned_tiles * epi;
+  return T0 + ucta * u + kF0 + kF1 * mt + epi;
 }
 
 static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force_ntok, int force_grid,
                             int force_split) {
   if (force_ntok > 0 || force_split >= 0 || force_grid > 0) {
     const int nt = force_ntok > 0 ? force_ntok : (M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256);
-    const bool sk = force_split >= 0 ? force_split == 1 : nt <= 64;
+    const int sk = force_split >= 0 ? force_split : (nt <= 64 ? 1 : 2);
     return plan_for(mode, M, N, K, nt, sk, force_grid);
   }
   LaunchPlan best{};
   double best_t = 1e30;
   for (int nt : {16, 32, 64, 128, 256}) {
     if (nt > 16 && nt / 2 >= M) break;  // a smaller tile already covers every token
-    for (int sk = 0; sk < 2; ++sk) {
-      const LaunchPlan lp = plan_for(mode, M, N, K, nt, sk == 1, 0);
+    for (int sk = 0; sk < 2; ++sk) {  // whole tiles / stream-K (the hybrid never won a sweep point)
+      const LaunchPlan lp = plan_for(mode, M, N, K, nt, sk, 0);
       if (lp.tiles > 65536) continue;
       const double t = plan_cost_us(lp, M);
       if (t < best_t) {
@@ -952,11 +1027,11 @@ template <int MODE>
 static int launch_mode(int ntok, const CUtensorMap& map, const CUtensorMap& ymap, const GemmParams& p, int grid,
                        cudaStream_t st) {
   switch (ntok) {
-    case 16: return launch_t<MODE, 16, bk_for(16)>(map, ymap, p, grid, st);
-    case 32: return launch_t<MODE, 32, bk_for(32)>(map, ymap, p, grid, st);
-    case 64: return launch_t<MODE, 64, bk_for(64)>(map, ymap, p, grid, st);
-    case 128: return launch_t<MODE, 128, bk_for(128)>(map, ymap, p, grid, st);
-    case 256: return launch_t<MODE, 256, bk_for(256)>(map, ymap, p, grid, st);
+    case 16: return launch_t<MODE, 16, bk_for(MODE, 16)>(map, ymap, p, grid, st);
+    case 32: return launch_t<MODE, 32, bk_for(MODE, 32)>(map, ymap, p, grid, st);
+    case 64: return launch_t<MODE, 64, bk_for(MODE, 64)>(map, ymap, p, grid, st);
+    case 128: return launch_t<MODE, 128, bk_for(MODE, 128)>(map, ymap, p, grid, st);
+    case 256: return launch_t<MODE, 256, bk_for(MODE, 256)>(map, ymap, p, grid, st);
     default: return kErrConfig;
   }
 }
@@ -969,7 +1044,7 @@ extern "C" size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   size_t best = 0;  // any plan a caller may force or the cost model may pick
   for (int nt : {16, 32, 64, 128, 256}) {
-    LaunchPlan lp = plan_for(kModePG, M, N, K, nt, true, 0);  // slots do not change the slot bytes
+    LaunchPlan lp = plan_for(kModePG, M, N, K, nt, 1, 0);  // slots do not change the slot bytes
     size_t b = plan_ws_bytes(lp);
     if (b > best) best = b;
   }
@@ -1052,6 +1127,8 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   p.max_segs = lp.max_segs;
   p.units = lp.units;
   p.aligned_tiles = lp.aligned_tiles;
+  p.dp_tiles = lp.dp_tiles;
+  p.sk_unit0 = lp.sk_unit0;
   p.dbg = cfg ? (unsigned long long*)cfg->dbg : nullptr;
 
   switch (mode) {

@@ -260,7 +260,7 @@ def test_gemm_m_sweep_vs_oracle(scheme, gs):
 
 
 @pytest.mark.parametrize("ntok", [16, 32, 64, 128, 256])
-@pytest.mark.parametrize("split", [0, 1])
+@pytest.mark.parametrize("split", [0, 1, 2])
 def test_gemm_all_tile_plans(ntok, split):
     m, k, n = 77, 2304, 640
     for scheme in ("per-channel", "per-group"):
