@@ -81,7 +81,10 @@ struct Cfg {
   // k-block so the per-k-block handshake cost (~80 instructions per warp) stays
   // well below the conversion work
   static constexpr int kNumConvWarps = kSmall ? 8 : QQQ_BIG_CONV_WARPS;
-  static constexpr int kNumEpiWarps = kSmall ? 4 : 8;  // 1 or 2 groups of 4 (one warp per lane quadrant)
+#ifndef QQQ_BIG_EPI_WARPS
+#define QQQ_BIG_EPI_WARPS 8
+#endif
+  static constexpr int kNumEpiWarps = kSmall ? 4 : QQQ_BIG_EPI_WARPS;  // groups of 4 (one warp per lane quadrant)
   static constexpr int kEpiGroups = kNumEpiWarps / 4;
   static constexpr int kConvWarp0 = 0;
   static constexpr int kEpiWarp0 = kNumConvWarps;
@@ -126,7 +129,7 @@ struct Cfg {
   static constexpr int kOffX = 0;  // 1024-aligned: NTOK*BK is a multiple of 2048
   static constexpr int kOffW = kOffX + kXStages * kXBytes;
   static constexpr int kOffBar = (kOffW + kWStages * kWBytes + 1023) / 1024 * 1024;
-  static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 4 + 4;
+  static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 4 + 2 * kEpiGroups;
   static constexpr int kOffSA = kOffBar + (kNumBars * 8 + 16 + 15) / 16 * 16;  // per-token scales of a tile (f64)
   static constexpr int kOffRS = kOffSA + NTOK * 8;                             // per-token code sums (int32)
   static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;  // per epilogue warp: 2 x [16 tok][32 ch] fp16
@@ -211,11 +214,21 @@ QQQ_DEVICE double i32_to_f64_exact(int32_t a) {
 
 // y = f16((acc * s_a[t]) * s_col) for 16 tokens of one channel, branch-free:
 // f64 with one final RN rounding (cvt.rn.f16.f64), as gemm.py:182-184/200-202.
-QQQ_DEVICE void dequant16(const uint32_t (&r)[16], const double* sa, double s_col, uint16_t (&h)[16]) {
+// (only the first nvalid tokens are converted: rows past M are never stored)
+QQQ_DEVICE void dequant16(const uint32_t (&r)[16], const double* sa, double s_col, uint16_t (&h)[16],
+                          int nvalid = 16) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    const double v = (i32_to_f64_exact((int32_t)r[i]) * sa[i]) * s_col;
-    h[i] = __half_as_ushort(f64_to_f16_rn(v));
+#ifdef QQQ_EXP_NO_DEQ
+    h[i] = (uint16_t)r[i];
+#else
+    if (i < nvalid) {
+      const double v = (i32_to_f64_exact((int32_t)r[i]) * sa[i]) * s_col;
+      h[i] = __half_as_ushort(f64_to_f16_rn(v));
+    } else {
+      h[i] = 0;
+    }
+#endif
   }
 }
 
@@ -312,6 +325,37 @@ QQQ_DEVICE int cta_of_unit(int64_t u, const GemmParams& p, int grid) {
   return (int)(((u - p.sk_unit0 + 1) * grid - 1) / p.units);
 }
 
+// Incremental (n_tile, token tile, k-block) cursor over consecutive units of a
+// stream-K range: one division at construction, none per step.
+struct UnitCursor {
+  int n_tile, tt, kb;
+  QQQ_DEVICE UnitCursor(const GemmParams& p, int64_t u) {
+    const int tile = (int)(u / p.kb_per_tile);
+    n_tile = tile / p.tok_tiles;
+    tt = tile % p.tok_tiles;
+    kb = (int)(u % p.kb_per_tile);
+  }
+  QQQ_DEVICE void adv(const GemmParams& p) {
+    if (++kb == p.kb_per_tile) {
+      kb = 0;
+      if (++tt == p.tok_tiles) {
+        tt = 0;
+        ++n_tile;
+      }
+    }
+  }
+};
+
+// one weight k-block (BK/128 super-slabs of one 128-channel tile) -> ring stage
+template <int BK>
+QQQ_DEVICE void issue_weight_kblock(const GemmParams& p, const UnitCursor& c, uint8_t* dst, uint64_t* bar) {
+  const int nss = min(BK / 128, p.ss_per_tile - c.kb * (BK / 128));
+  const uint32_t wbytes = (uint32_t)(nss * p.ss_bytes);
+  const int64_t ss0 = (int64_t)c.n_tile * p.ss_per_tile + (int64_t)c.kb * (BK / 128);
+  mbar_arrive_expect_tx(bar, wbytes);
+  bulk_g2s(dst, p.w + ss0 * p.ss_bytes, wbytes, bar);
+}
+
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
@@ -329,7 +373,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
   uint64_t* w_empty = w_full + C::kWStages;
   uint64_t* acc_full = w_empty + C::kWStages;
   uint64_t* acc_empty = acc_full + 2;
-  uint64_t* part_full = acc_empty + 2;  // [half][2]
+  uint64_t* part_full = acc_empty + 2;  // [group][2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
   const int warp = threadIdx.x >> 5;
@@ -342,19 +386,41 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
       mbar_init(&kb_full[s], C::kConvert ? C::kNumConvWarps + 1 : 1);
       mbar_init(&kb_empty[s], 1);
     }
-    for (int s = 0; s < C::kWStages; ++s) {
-      mbar_init(&w_full[s], 1);
-      mbar_init(&w_empty[s], C::kConvert ? C::kNumConvWarps : 1);
+    if (!C::kSmall) {  // small CTAs: the producer warp owns (and initialises) its weight ring
+      for (int s = 0; s < C::kWStages; ++s) {
+        mbar_init(&w_full[s], 1);
+        mbar_init(&w_empty[s], C::kConvert ? C::kNumConvWarps : 1);
+      }
     }
     for (int j = 0; j < C::kAccBufs; ++j) {
       mbar_init(&acc_full[j], 1);
       mbar_init(&acc_empty[j], C::kNumEpiWarps);
     }
-    for (int i = 0; i < 4; ++i) mbar_init(&part_full[i], 1);
+    for (int i = 0; i < 2 * C::kEpiGroups; ++i) mbar_init(&part_full[i], 1);
     mbar_fence_init();
   }
   if (warp == C::kActProducerWarp && lane == 0) tma_prefetch_desc(&act_map);
   if (warp == C::kAllocWarp) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (C::kSmall && warp == C::kWProducerWarp) {
+    // The first weight copies do not wait for the CTA set-up (TMEM allocation,
+    // other barriers): the decode critical path starts with this HBM latency.
+    if (lane == 0) {
+      for (int s = 0; s < C::kWStages; ++s) {
+        mbar_init(&w_full[s], 1);
+        mbar_init(&w_empty[s], C::kNumConvWarps);
+      }
+      mbar_fence_init();
+    }
+    __syncwarp();
+    SegIter si0 = make_iter(p);
+    const int total = (int)si0.total();
+    UnitCursor c(p, si0.u);
+    for (int i = 0; i < C::kWStages && i < total; ++i) {
+      if (elect_one()) issue_weight_kblock<BK>(p, c, smem + C::kOffW + i * C::kWBytes, &w_full[i]);
+      __syncwarp();
+      c.adv(p);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -374,33 +440,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
     // never depend on the previous kernel).
     SegIter si = make_iter(p);
     const int total = (int)si.total();  // small CTAs: a single stream-K range (no data-parallel part)
-    // incremental (n_tile, token tile, k-block) cursors: no division in the loop
-    struct Cur {
-      int n_tile, tt, kb;
-    };
-    auto adv = [&](Cur& c) {
-      if (++c.kb == p.kb_per_tile) {
-        c.kb = 0;
-        if (++c.tt == p.tok_tiles) {
-          c.tt = 0;
-          ++c.n_tile;
-        }
-      }
-    };
-    const int tile0 = (int)(si.u / p.kb_per_tile);
-    Cur wc{tile0 / p.tok_tiles, tile0 % p.tok_tiles, (int)(si.u % p.kb_per_tile)};
-    Cur xc = wc;
+    UnitCursor wc(p, si.u), xc = wc;
     uint32_t wi = 0, xi = 0;  // ring slots of the next copies
     auto issue_w = [&]() {
-      if (elect_one()) {
-        const int nss = min(BK / 128, p.ss_per_tile - wc.kb * (BK / 128));
-        const uint32_t wbytes = (uint32_t)(nss * p.ss_bytes);
-        const int64_t ss0 = (int64_t)wc.n_tile * p.ss_per_tile + (int64_t)wc.kb * (BK / 128);
-        mbar_arrive_expect_tx(&w_full[wi], wbytes);
-        bulk_g2s(smem + C::kOffW + wi * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &w_full[wi]);
-      }
+      if (elect_one()) issue_weight_kblock<BK>(p, wc, smem + C::kOffW + wi * C::kWBytes, &w_full[wi]);
       __syncwarp();
-      adv(wc);
+      wc.adv(p);
       if (++wi == C::kWStages) wi = 0;
     };
     auto issue_x = [&]() {
@@ -409,10 +454,14 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
         tma_load_3d(smem + C::kOffX + xi * C::kXBytes, &act_map, 0, xc.tt * NTOK, xc.kb * (BK / 128), &kb_full[xi]);
       }
       __syncwarp();
-      adv(xc);
+      xc.adv(p);
       if (++xi == C::kXStages) xi = 0;
     };
-    for (int i = 0; i < C::kWStages && i < total; ++i) issue_w();
+    // the weight prologue was issued before the set-up barrier: advance past it
+    for (int i = 0; i < C::kWStages && i < total; ++i) {
+      wc.adv(p);
+      if (++wi == C::kWStages) wi = 0;
+    }
     griddep_wait();  // the int8 activations come from the previous kernel
     for (int i = 0; i < C::kXStages && i < total; ++i) issue_x();
     uint32_t ws = 0, wph = 0, xs = 0, xph = 0;
@@ -816,7 +865,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
             // (OOB rows/cols clipped): no cross-warp barrier on the store path
             uint16_t* stg = reinterpret_cast<uint16_t*>(ystage) + (ych & 1) * 512;
             uint16_t h[16];
-            dequant16(r, sa_smem + c0, s_col, h);
+            dequant16(r, sa_smem + c0, s_col, h, tvalid - c0);
             if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer two chunks ago has read it
             __syncwarp();
 #pragma unroll

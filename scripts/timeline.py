@@ -30,6 +30,7 @@ ap.add_argument("--shape", default="4096x11008")
 ap.add_argument("--m", type=int, default=16)
 ap.add_argument("--scheme", default="per-group")
 ap.add_argument("--cfg", default="{}")
+ap.add_argument("--pair", action="store_true", help="two back-to-back launches (PDL overlap); report both")
 a = ap.parse_args()
 k, n = map(int, a.shape.split("x"))
 dev = torch.device("cuda", 0)
@@ -38,13 +39,43 @@ x = torch.randn((a.m, k), dtype=torch.float16, device=dev)
 aq = Q.quant_act_per_token(x)
 y = torch.empty((a.m, n), dtype=torch.float16, device=dev)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+prep2 = G.PreparedWeights(prep.mode, prep.w.clone(), None if prep.sc is None else prep.sc.clone(), prep.group,
+                           prep.s_col.clone())
+dbg = torch.zeros((1024, 192), dtype=torch.int64, device=dev)
+dbg2 = torch.zeros((1024, 192), dtype=torch.int64, device=dev)
+def launch():
+    G.run_gemm(aq, prep, n, False, y_out=y, cfg=dict(json.loads(a.cfg), dbg=dbg))
+    if a.pair:
+        G.run_gemm(aq, prep2, n, False, y_out=y, cfg=dict(json.loads(a.cfg), dbg=dbg2))
+launch()
+torch.cuda.synchronize()
+graph = torch.cuda.CUDAGraph()  # the pair is replayed from a graph: no host gap, PDL edges kept
+with torch.cuda.graph(graph):
+    launch()
 for rep in range(3):
-    dbg = torch.zeros((1024, 192), dtype=torch.int64, device=dev)
-    cfg = dict(json.loads(a.cfg), dbg=dbg)
+    dbg.zero_()
+    dbg2.zero_()
     flush.zero_()
     torch.cuda.synchronize()
-    G.run_gemm(aq, prep, n, False, y_out=y, cfg=cfg)
+    graph.replay()
     torch.cuda.synchronize()
+if a.pair:
+    d1 = dbg.cpu().numpy().astype(np.int64)
+    d2 = dbg2.cpu().numpy().astype(np.int64)
+    t0 = d1[d1[:, 0] > 0, 0].min()
+    for name, d in (("first", d1), ("second", d2)):
+        d = d[d[:, 0] > 0]
+        st = (d[:, 0] - t0) / 1e3
+        en = (d[:, 63] - t0) / 1e3
+        print(f"{name}: ctas={len(d)} start min/med/max {st.min():.2f}/{np.median(st):.2f}/{st.max():.2f}  "
+              f"end min/med/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f}  "
+              f"dep_wait med {np.median((d[:, 3] - t0) / 1e3):.2f}")
+        for sl, nm in ((4, "full0"), (96, "mma_xfull0"), (20, "mma0")):
+            v = d[:, sl]
+            v = v[v > 0]
+            if v.size:
+                print(f"   {nm}: min/med/max {((v - t0) / 1e3).min():.2f}/{np.median((v - t0) / 1e3):.2f}/{((v - t0) / 1e3).max():.2f}")
+    sys.exit(0)
 d = dbg.cpu().numpy().astype(np.int64)
 ctas = d[:, 0] > 0
 d = d[ctas]
