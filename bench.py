@@ -267,6 +267,47 @@ def graph_time_us(fns, reps, warm=2):
     return s.elapsed_time(e) * 1e3 / (reps * len(fns))
 
 
+def extra_points(peaks, dev, specs):
+    """Supplementary device-time points outside the contract workload: BASELINE
+    configs[0] (C1, per-channel M=16, N=K=4096) and configs[2] (C3, Llama-2-70B
+    shapes, per-channel vs per-group). Same method as roofline_points: CUDA
+    graph over rotated cold weight replicas, fp16 cuBLAS with cold weights."""
+    import torch
+
+    import paper_2406_09904_b200 as Q
+    from paper_2406_09904_b200 import gemm as G
+
+    int8_peak = 2.0 * peaks["bf16_tflops"]
+    out = []
+    for (k, n, scheme, ms) in specs:
+        qw, fused, prep = make_weights(k, n, scheme, seed=77, device=dev)
+        R = max(2, math.ceil(2.5 * L2_BYTES / (k * n / 2)))
+        reps = [prep] + [G.PreparedWeights(prep.mode, prep.w.clone(), None if prep.sc is None else prep.sc.clone(),
+                                           prep.group, prep.s_col.clone()) for _ in range(R - 1)]
+        r16 = max(2, math.ceil(2.5 * L2_BYTES / (k * n * 2)))
+        w16 = [torch.randn((k, n), dtype=torch.float16, device=dev) for _ in range(r16)]
+        for m in ms:
+            x = torch.randn((m, k), dtype=torch.float16, device=dev)
+            aq = Q.quant_act_per_token(x)
+            y = torch.empty((m, n), dtype=torch.float16, device=dev)
+            G.workspace(dev, Q._lib.load().qqq_gemm_workspace_bytes(m, n, k))
+            fns = [(lambda p_: (lambda: G.run_gemm(aq, p_, n, False, y_out=y)))(p_) for p_ in reps]
+            t_us = graph_time_us(fns, reps=max(2, 40 // R))
+            t16 = graph_time_us([(lambda wi: (lambda: torch.matmul(x, wi)))(wi) for wi in w16],
+                                reps=max(2, 40 // len(w16)))
+            ops = 2.0 * m * n * k
+            byts = alg_bytes(m, k, n, scheme)
+            t_hbm = byts / (peaks["hbm_gbs"] * 1e3)
+            t_ten = ops / (int8_peak * 1e6)
+            out.append(dict(shape=f"{k}x{n}", scheme=scheme, M=m, us=round(t_us, 3), TOPS=round(ops / t_us / 1e6, 2),
+                            GBps=round(byts / t_us / 1e3, 1), bound="hbm" if t_hbm >= t_ten else "tensor",
+                            frac=round(max(t_hbm, t_ten) / t_us, 4), fp16_us=round(t16, 3),
+                            speedup_vs_fp16=round(t16 / t_us, 3)))
+        del reps, w16
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_gpu_arm(args, world, rank, local):
     import numpy as np
     import torch
@@ -338,6 +379,14 @@ def run_gpu_arm(args, world, rank, local):
                            GBps=round(byts / t_us / 1e3, 1), bound=bound,
                            frac=round(max(t_hbm, t_ten) / t_us, 4), fp16_us=round(t16, 3),
                            speedup_vs_fp16=round(t16 / t_us, 3)))
+
+    # ---- supplementary configs (not part of the contract number) ---------------
+    c1_points, c3_points = None, None
+    if not args.quick and rank == 0:
+        c1_points = extra_points(peaks, dev, [(4096, 4096, "per-channel", [16])])
+        c3_points = extra_points(peaks, dev, [(k, n, sch, [1, 16, 1024]) for (k, n) in
+                                             [(8192, 8192), (8192, 28672), (28672, 8192)]
+                                             for sch in ("per-channel", "per-group")])
 
     # ---- the contract timed region: K steps of the 33-GEMM sweep ---------------
     g = torch.cuda.CUDAGraph()
@@ -422,6 +471,8 @@ def run_gpu_arm(args, world, rank, local):
                                    sweep_speedup=round(f16_total / ours_total, 3),
                                    min_point_speedup=min(p["speedup_vs_fp16"] for p in points)),
                 roofline_points=points,
+                c1_points=c1_points,
+                c3_points=c3_points,
                 gpu_launches=len(order) * args.steps,
                 clocks=clk.summary())
     if e2e:

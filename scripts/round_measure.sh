@@ -8,17 +8,20 @@ if [ -z "$NOTEST" ]; then
   timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
   echo "smoke exit $?" >> gpurun_out/smoke.log
 fi
-timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
-echo "bench exit $?" >> gpurun_out/bench.err
+if [ -z "$NOBENCH" ]; then
+  timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
+  echo "bench exit $?" >> gpurun_out/bench.err
+fi
 if [ -z "$NONCU" ]; then
   # launch list of the bench command (cold, serialised: compare shares)
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-      python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
-  # full capture of the dominant kernel: prefill (M=1024) and decode (M=16) points
-  for spec in "4096x11008 1024" "4096x11008 16"; do
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+      python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --quick > gpurun_out/ncu_bench.log 2>&1
+  echo "ncu launch list exit $?" >> gpurun_out/ncu_bench.log
+  # full captures of the dominant kernel at decode / mid / prefill M
+  for spec in "4096x11008 1024" "4096x11008 128" "4096x11008 16" "4096x11008 1"; do
     set -- $spec
     timeout 300 ncu --set full --import-source on --clock-control none -k regex:w4a8_gemm -s 2 -c 1 \
         -o gpurun_out/prof_$1_m$2 -f python scripts/quick_bench.py --profile --shapes $1 --ms $2 > gpurun_out/ncu_$1_m$2.log 2>&1
   done
 fi
-tail -3 gpurun_out/pytest_gpu.log 2>/dev/null; tail -1 gpurun_out/smoke.log 2>/dev/null; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
+tail -3 gpurun_out/pytest_gpu.log 2>/dev/null; tail -1 gpurun_out/smoke.log 2>/dev/null; tail -c 600 gpurun_out/bench.json; tail -3 gpurun_out/bench.err; tail -2 gpurun_out/ncu_bench.log
