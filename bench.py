@@ -308,6 +308,59 @@ def extra_points(peaks, dev, specs):
     return out
 
 
+C4_LINEARS = [("qkv", 4096, 12288), ("o", 4096, 4096), ("gate_up", 4096, 22016), ("down", 11008, 4096)]
+
+
+def c4_stack_points(peaks, dev, batches=(1, 16, 64, 256)):
+    """BASELINE configs[3] (C4): the Llama-2-7B decoder-layer linear stack
+    (QKV 4096->12288, O 4096->4096, gate-up 4096->22016, down 11008->4096),
+    each linear = fused smooth-divide + per-token act quant (apply_quant_linear's
+    activation step, pipeline.py:146) + per-group g=128 W4A8 GEMM, the 8
+    launches of a stack chained with PDL in one CUDA graph; weights cold
+    (rotated layer replicas). Compared with the fp16 torch.matmul stack."""
+    import torch
+
+    import paper_2406_09904_b200 as Q
+    from paper_2406_09904_b200 import gemm as G
+
+    layer_bytes = sum(k * n / 2 for _, k, n in C4_LINEARS)
+    R = max(2, math.ceil(2.5 * L2_BYTES / layer_bytes))
+    layers = []
+    for r in range(R):
+        lin = []
+        for li, (name, k, n) in enumerate(C4_LINEARS):
+            qw, fused, prep = make_weights(k, n, "per-group", seed=500 + 10 * r + li, device=dev)
+            sm = torch.ones(k, dtype=torch.float64, device=dev)
+            idx = torch.randperm(k, device=dev)[: k // 8]
+            sm[idx] = 0.5 + 1.5 * torch.rand(k // 8, dtype=torch.float64, device=dev)
+            lin.append((k, n, prep, sm))
+        layers.append(lin)
+    r16 = max(2, math.ceil(2.5 * L2_BYTES / (4 * layer_bytes)))
+    w16 = [[torch.randn((k, n), dtype=torch.float16, device=dev) for _, k, n in C4_LINEARS] for _ in range(r16)]
+    ops_stack = lambda m: sum(2.0 * m * k * n for _, k, n in C4_LINEARS)
+    out = []
+    for m in batches:
+        xs = [torch.randn((m, k), dtype=torch.float16, device=dev) for _, k, _n in C4_LINEARS]
+        ys = [torch.empty((m, n), dtype=torch.float16, device=dev) for _, _k, n in C4_LINEARS]
+        G.workspace(dev, max(Q._lib.load().qqq_gemm_workspace_bytes(m, n, k) for _, k, n in C4_LINEARS))
+
+        def stack_fn(lin):
+            def f():
+                for i, (k, n, prep, sm) in enumerate(lin):
+                    aq = Q.quant_act_smoothed(xs[i], sm, check=False)
+                    G.run_gemm(aq, prep, n, False, y_out=ys[i])
+            return f
+
+        t_us = graph_time_us([stack_fn(lin) for lin in layers], reps=max(2, 20 // R))
+        t16 = graph_time_us([(lambda ws: (lambda: [torch.matmul(xs[i], ws[i]) for i in range(4)]))(ws) for ws in w16],
+                            reps=max(2, 20 // r16))
+        out.append(dict(batch=m, us_per_stack=round(t_us, 2), TOPS=round(ops_stack(m) / t_us / 1e6, 2),
+                        fp16_us=round(t16, 2), speedup_vs_fp16=round(t16 / t_us, 3)))
+    del layers, w16
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_gpu_arm(args, world, rank, local):
     import numpy as np
     import torch
@@ -381,8 +434,9 @@ def run_gpu_arm(args, world, rank, local):
                            speedup_vs_fp16=round(t16 / t_us, 3)))
 
     # ---- supplementary configs (not part of the contract number) ---------------
-    c1_points, c3_points = None, None
+    c1_points, c3_points, c4_points = None, None, None
     if not args.quick and rank == 0:
+        c4_points = c4_stack_points(peaks, dev)
         c1_points = extra_points(peaks, dev, [(4096, 4096, "per-channel", [16])])
         c3_points = extra_points(peaks, dev, [(k, n, sch, [1, 16, 1024]) for (k, n) in
                                              [(8192, 8192), (8192, 28672), (28672, 8192)]
@@ -473,6 +527,7 @@ def run_gpu_arm(args, world, rank, local):
                 roofline_points=points,
                 c1_points=c1_points,
                 c3_points=c3_points,
+                c4_points=c4_points,
                 gpu_launches=len(order) * args.steps,
                 clocks=clk.summary())
     if e2e:

@@ -59,6 +59,12 @@ int qqq_act_quant(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx,
  * GEMM needs (its weights run as u8 = w8 + 128; acc = acc_u8 - 128*rowsum). */
 int qqq_act_quant_ex(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
                      double* s_a, int32_t* rowsum, int32_t* status_dev, qqq_stream_t stream);
+/* apply_quant_linear's activation step (pipeline.py:146): quant_act_per_token
+ * of x / smooth, smooth = the smoothing plan's f64[K] vector (smoothing.py:38-43),
+ * divided in f64 inside the quantizer (replaces the numpy divide + quantize). */
+int qqq_act_quant_smooth(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, const double* smooth,
+                         int8_t* q, int64_t ldq, double* s_a, int32_t* rowsum, int32_t* status_dev,
+                         qqq_stream_t stream);
 /* rowsum of existing int8 codes (activations not produced by qqq_act_quant_ex). */
 int qqq_act_rowsum(const int8_t* q, int64_t M, int64_t K, int64_t ldq, int32_t* rowsum, qqq_stream_t stream);
 

@@ -68,14 +68,19 @@ QQQ_DEVICE Acc block_max(Acc v, Acc* red) {
   return red[0];
 }
 
-template <typename T, int kThreads>
+// kSmooth: the reference's apply_quant_linear (pipeline.py:144-152) quantizes
+// x / s with the smoothing vector s (f64, per input channel) divided in f64
+// first: every element is then an f64 value, so absmax and codes use the
+// verbatim f64 formula (IEEE division, as numpy).
+template <typename T, int kThreads, bool kSmooth = false>
 __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict__ x, int64_t K, int64_t ldx,
                                                               int8_t* __restrict__ q, int64_t ldq,
                                                               double* __restrict__ s_out, int32_t* status,
                                                               const double* __restrict__ row_max_in,
                                                               double* __restrict__ row_max_out,
-                                                              int32_t* __restrict__ rowsum_out) {
-  using Acc = typename std::conditional<sizeof(T) == 8, double, float>::type;
+                                                              int32_t* __restrict__ rowsum_out,
+                                                              const double* __restrict__ smooth = nullptr) {
+  using Acc = typename std::conditional<sizeof(T) == 8 || kSmooth, double, float>::type;
   __shared__ Acc red[32];
   // PDL: let the GEMM that consumes q start its prologue / weight prefetch now,
   // and wait for whatever produced x before reading it.
@@ -98,14 +103,24 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
       const T* e = reinterpret_cast<const T*>(&pk);
 #pragma unroll
       for (int j = 0; j < kVec; ++j) {
-        Acc a = absval(e[j]);
+        Acc a;
+        if constexpr (kSmooth) {
+          a = fabs(to_f64<T>(e[j]) / smooth[i * kVec + j]);
+        } else {
+          a = absval(e[j]);
+        }
         bad |= is_bad(a);  // inf or NaN
         m = a > m ? a : m;
       }
     }
   } else {
     for (int64_t i = threadIdx.x; i < K; i += kThreads) {
-      Acc a = absval(xr[i]);
+      Acc a;
+      if constexpr (kSmooth) {
+        a = fabs(to_f64<T>(xr[i]) / smooth[i]);
+      } else {
+        a = absval(xr[i]);
+      }
       bad |= is_bad(a);
       m = a > m ? a : m;
     }
@@ -125,9 +140,11 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
   // ---- pass 2: codes ----------------------------------------------------------------
   const bool zero_row = !(m > Acc(0));
   const float inv = zero_row ? 0.0f : 127.0f / (float)m;  // fp16 path only
-  auto code = [&](T v) -> int8_t {
+  auto code = [&](T v, int64_t k) -> int8_t {
     if (zero_row) return 0;
-    if constexpr (sizeof(T) == 2) {
+    if constexpr (kSmooth) {
+      return quant_code_exact(to_f64<T>(v) / smooth[k], s);
+    } else if constexpr (sizeof(T) == 2) {
       return quant_code_f16(__half2float(v), inv, s);
     } else {
       return quant_code_exact(to_f64<T>(v), s);
@@ -146,7 +163,7 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
         const T* e = reinterpret_cast<const T*>(&pk);
 #pragma unroll
         for (int j = 0; j < kVec; ++j) {
-          out[h * kVec + j] = code(e[j]);
+          out[h * kVec + j] = code(e[j], i * 16 + h * kVec + j);
           csum += out[h * kVec + j];
         }
       }
@@ -154,7 +171,7 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
     }
   } else {
     for (int64_t i = threadIdx.x; i < K; i += kThreads) {
-      const int8_t c = code(xr[i]);
+      const int8_t c = code(xr[i], i);
       qr[i] = c;
       csum += c;
     }
@@ -194,7 +211,7 @@ using namespace qqq;
 
 static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
                             double* s_a, int32_t* status_dev, const double* row_max_in, double* row_max_out,
-                            int32_t* rowsum, cudaStream_t stream) {
+                            int32_t* rowsum, cudaStream_t stream, const double* smooth = nullptr) {
   if (M < 0 || K <= 0 || ldx < K || (!row_max_out && ldq < K)) return kErrShape;
   if (M == 0) return kOk;
   constexpr int kT = 256;
@@ -208,18 +225,38 @@ static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, in
   lc.attrs = attr;
   lc.numAttrs = 1;
   cudaError_t e;
+  if (smooth) {
+    if (row_max_in || row_max_out) return kErrConfig;
+    switch (x_dtype) {
+      case 0:
+        e = cudaLaunchKernelEx(&lc, act_quant_kernel<__half, kT, true>, (const __half*)x, K, ldx, q, ldq, s_a,
+                               status_dev, row_max_in, row_max_out, rowsum, smooth);
+        break;
+      case 1:
+        e = cudaLaunchKernelEx(&lc, act_quant_kernel<float, kT, true>, (const float*)x, K, ldx, q, ldq, s_a,
+                               status_dev, row_max_in, row_max_out, rowsum, smooth);
+        break;
+      case 2:
+        e = cudaLaunchKernelEx(&lc, act_quant_kernel<double, kT, true>, (const double*)x, K, ldx, q, ldq, s_a,
+                               status_dev, row_max_in, row_max_out, rowsum, smooth);
+        break;
+      default:
+        return kErrConfig;
+    }
+    return e == cudaSuccess ? kOk : kErrCuda;
+  }
   switch (x_dtype) {
     case 0:
       e = cudaLaunchKernelEx(&lc, act_quant_kernel<__half, kT>, (const __half*)x, K, ldx, q, ldq, s_a, status_dev,
-                             row_max_in, row_max_out, rowsum);
+                             row_max_in, row_max_out, rowsum, nullptr);
       break;
     case 1:
       e = cudaLaunchKernelEx(&lc, act_quant_kernel<float, kT>, (const float*)x, K, ldx, q, ldq, s_a, status_dev,
-                             row_max_in, row_max_out, rowsum);
+                             row_max_in, row_max_out, rowsum, nullptr);
       break;
     case 2:
       e = cudaLaunchKernelEx(&lc, act_quant_kernel<double, kT>, (const double*)x, K, ldx, q, ldq, s_a, status_dev,
-                             row_max_in, row_max_out, rowsum);
+                             row_max_in, row_max_out, rowsum, nullptr);
       break;
     default:
       return kErrConfig;
@@ -255,4 +292,13 @@ extern "C" int qqq_act_quant_with_max(const void* x, int x_dtype, int64_t M, int
                                       int32_t* status_dev, cudaStream_t stream) {
   if (!row_max) return kErrConfig;
   return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, row_max, nullptr, rowsum, stream);
+}
+
+// apply_quant_linear's activation step (pipeline.py:146): quant_act_per_token
+// of x / s, the f64 division fused into the quantizer (one pass over x).
+extern "C" int qqq_act_quant_smooth(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx,
+                                    const double* smooth, int8_t* q, int64_t ldq, double* s_a, int32_t* rowsum,
+                                    int32_t* status_dev, cudaStream_t stream) {
+  if (!smooth) return kErrConfig;
+  return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, nullptr, nullptr, rowsum, stream, smooth);
 }

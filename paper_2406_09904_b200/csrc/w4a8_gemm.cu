@@ -75,7 +75,7 @@ struct Cfg {
   static constexpr bool kSmall = NTOK <= 64 && MODE != kModeI8;  // (I8 stages are 2x larger)
   static constexpr int kCtasPerSm = kSmall ? 2 : 1;
 #ifndef QQQ_BIG_CONV_WARPS
-#define QQQ_BIG_CONV_WARPS 8
+#define QQQ_BIG_CONV_WARPS 16
 #endif
   // 2 per TMEM lane quadrant: each converter warp handles >= 2 slabs per
   // k-block so the per-k-block handshake cost (~80 instructions per warp) stays

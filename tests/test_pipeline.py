@@ -1,0 +1,78 @@
+"""apply_quant_linear (pipeline.py:144-152): the CPU oracle against golden
+vectors made by the reference itself (tests/golden/make_golden_pipeline.py),
+and (GPU) the fused smooth+quantize kernel and the B200 linear against the
+same vectors — bit-exact (codes, f64 scales, y widened to f64)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import qqq_oracle as O
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "pipeline_cases.npz")
+
+
+def _cases():
+    g = np.load(GOLD)
+    for i in range(int(g["n_cases"])):
+        p = f"c{i}_"
+        t, k, n, gs, pg, f16 = (int(v) for v in g[p + "meta"])
+        yield dict(i=i, t=t, k=k, n=n, gs=gs, pg=bool(pg), f16=bool(f16), x=g[p + "x"], s=g[p + "s"],
+                   packed=g[p + "packed"], s_w=g.get(p + "s_w"), s_wg=g.get(p + "s_wg"), s_wc=g.get(p + "s_wc"),
+                   q=g[p + "q"], s_a=g[p + "s_a"], y=g[p + "y"])
+
+
+def _oracle_qw(c):
+    if c["pg"]:
+        return O.QuantizedWeights(c["packed"], c["k"], c["n"], O.PER_GROUP, c["gs"], s_wg=c["s_wg"], s_wc=c["s_wc"])
+    return O.QuantizedWeights(c["packed"], c["k"], c["n"], O.PER_CHANNEL, s_w=c["s_w"])
+
+
+def test_oracle_apply_quant_linear_matches_reference_goldens():
+    for c in _cases():
+        qa = O.quant_act_per_token(c["x"] / c["s"][None, :])
+        assert np.array_equal(qa.q, c["q"]) and np.array_equal(qa.s_a.view(np.uint64), c["s_a"].view(np.uint64))
+        y = O.apply_quant_linear(c["x"], c["s"], _oracle_qw(c))
+        assert np.array_equal(y.view(np.uint64), c["y"].view(np.uint64)), c["i"]
+
+
+@pytest.mark.gpu
+def test_gpu_apply_quant_linear_bit_exact():
+    import torch
+
+    import paper_2406_09904_b200 as Q
+
+    dev = torch.device("cuda")
+    f = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    for c in _cases():
+        qw = (Q.QuantizedWeights(f(c["packed"]), c["k"], c["n"], Q.PER_GROUP, c["gs"], s_wg=f(c["s_wg"]),
+                                 s_wc=f(c["s_wc"])) if c["pg"]
+              else Q.QuantizedWeights(f(c["packed"]), c["k"], c["n"], Q.PER_CHANNEL, s_w=f(c["s_w"])))
+        plan = Q.SmoothingPlan(sigma=1.0, selected=(), s=c["s"], objective=0.0)
+        layer = Q.QuantizedLayer(name=f"case{c['i']}", qweights=qw, plan=plan)
+        # fp16 activations arrive as fp16 tensors when they are fp16-exact, else as f64
+        x = torch.from_numpy(c["x"]).to(dev)
+        if c["f16"]:
+            x = x.to(torch.float16)
+        qa = Q.quant_act_smoothed(x, c["s"])
+        assert np.array_equal(qa.q.cpu().numpy(), c["q"]), c["i"]
+        assert np.array_equal(qa.s_a.cpu().numpy().view(np.uint64), c["s_a"].view(np.uint64)), c["i"]
+        y = Q.apply_quant_linear(x, layer)
+        assert y.dtype == torch.float64
+        assert np.array_equal(y.cpu().numpy().view(np.uint64), c["y"].view(np.uint64)), c["i"]
+
+
+@pytest.mark.gpu
+def test_gpu_apply_quant_linear_errors():
+    import torch
+
+    import paper_2406_09904_b200 as Q
+
+    dev = torch.device("cuda")
+    x = torch.randn(4, 128, device=dev, dtype=torch.float16)
+    with pytest.raises(Q.ShapeError):
+        Q.quant_act_smoothed(x, np.ones(64))
+    x[1, 3] = float("inf")
+    with pytest.raises(Q.DataError):
+        Q.quant_act_smoothed(x, np.ones(128))
