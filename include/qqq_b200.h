@@ -61,10 +61,13 @@ int qqq_act_quant_ex(const void* x, int x_dtype, int64_t M, int64_t K, int64_t l
                      double* s_a, int32_t* rowsum, int32_t* status_dev, qqq_stream_t stream);
 /* apply_quant_linear's activation step (pipeline.py:146): quant_act_per_token
  * of x / smooth, smooth = the smoothing plan's f64[K] vector (smoothing.py:38-43),
- * divided in f64 inside the quantizer (replaces the numpy divide + quantize). */
+ * divided in f64 inside the quantizer (replaces the numpy divide + quantize).
+ * smooth_mask (optional, may be NULL): ceil(K/8) bytes, bit k set <=> smooth[k]
+ * != 1.0 — channels outside the plan's `selected` set skip the f64 division
+ * (and the load of smooth[k]); results are identical either way. */
 int qqq_act_quant_smooth(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, const double* smooth,
-                         int8_t* q, int64_t ldq, double* s_a, int32_t* rowsum, int32_t* status_dev,
-                         qqq_stream_t stream);
+                         const uint8_t* smooth_mask, int8_t* q, int64_t ldq, double* s_a, int32_t* rowsum,
+                         int32_t* status_dev, qqq_stream_t stream);
 /* rowsum of existing int8 codes (activations not produced by qqq_act_quant_ex). */
 int qqq_act_rowsum(const int8_t* q, int64_t M, int64_t K, int64_t ldq, int32_t* rowsum, qqq_stream_t stream);
 

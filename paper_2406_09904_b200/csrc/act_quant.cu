@@ -42,6 +42,20 @@ QQQ_DEVICE int8_t quant_code_exact(double x, double s) {
   return (int8_t)(int)r;
 }
 
+// Same result as quant_code_exact without the f64 division on the common path:
+// inv = RN(1/s); |x*inv - x/s| <= 2^-51 * 127, so rint agrees unless x/s is
+// within 1e-9 of a half-integer, where the verbatim division decides.
+QQQ_DEVICE int8_t quant_code_f64(double x, double inv, double s) {
+  const double u = x * inv;
+  const double r = rint(u);
+  if (fabs(fabs(u - r) - 0.5) < 1e-9) return quant_code_exact(x, s);
+  return (int8_t)(int)fmin(fmax(r, -127.0), 127.0);
+}
+
+// the smoothed activation x / s_k (pipeline.py:146, f64 IEEE division); most
+// channels are not smoothed (s_k == 1.0, x / 1.0 == x exactly)
+QQQ_DEVICE double smooth_div(double x, double sk) { return sk == 1.0 ? x : x / sk; }
+
 // fp16 fast path; inv = RN(127/m) in fp32 (m = row absmax > 0), s the f64
 // scale. |x*inv - x*127/m| <= 2*127*2^-24 < 2e-5, far inside the 1e-3 band.
 QQQ_DEVICE int8_t quant_code_f16(float x, float inv, double s) {
@@ -105,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
       for (int j = 0; j < kVec; ++j) {
         Acc a;
         if constexpr (kSmooth) {
-          a = fabs(to_f64<T>(e[j]) / smooth[i * kVec + j]);
+          a = fabs(smooth_div(to_f64<T>(e[j]), smooth[i * kVec + j]));
         } else {
           a = absval(e[j]);
         }
@@ -117,7 +131,7 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
     for (int64_t i = threadIdx.x; i < K; i += kThreads) {
       Acc a;
       if constexpr (kSmooth) {
-        a = fabs(to_f64<T>(xr[i]) / smooth[i]);
+        a = fabs(smooth_div(to_f64<T>(xr[i]), smooth[i]));
       } else {
         a = absval(xr[i]);
       }
@@ -140,10 +154,11 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
   // ---- pass 2: codes ----------------------------------------------------------------
   const bool zero_row = !(m > Acc(0));
   const float inv = zero_row ? 0.0f : 127.0f / (float)m;  // fp16 path only
+  const double inv64 = 1.0 / s;                            // smoothed (f64) path
   auto code = [&](T v, int64_t k) -> int8_t {
     if (zero_row) return 0;
     if constexpr (kSmooth) {
-      return quant_code_exact(to_f64<T>(v) / smooth[k], s);
+      return quant_code_f64(smooth_div(to_f64<T>(v), smooth[k]), inv64, s);
     } else if constexpr (sizeof(T) == 2) {
       return quant_code_f16(__half2float(v), inv, s);
     } else {
@@ -189,6 +204,110 @@ __global__ void __launch_bounds__(kThreads) act_quant_kernel(const T* __restrict
   }
 }
 
+// Register-resident variant for rows that fit in one CTA's registers (fp16
+// input, K <= kThreads * kVPT * 8): every thread issues its kVPT 16-byte loads
+// up front (one HBM/L2 round trip per row instead of one per loop trip), the
+// row max is one warp-shuffle + shared-memory reduction, and the codes are
+// computed from the registers (no second pass over x). Same arithmetic as
+// act_quant_kernel, so the same bit-exactness argument holds.
+template <int kThreads, int kVPT, bool kSmooth>
+__global__ void __launch_bounds__(kThreads) act_quant_row_kernel(const __half* __restrict__ x, int64_t K, int64_t ldx,
+                                                                  int8_t* __restrict__ q, int64_t ldq,
+                                                                  double* __restrict__ s_out, int32_t* status,
+                                                                  int32_t* __restrict__ rowsum_out,
+                                                                  const double* __restrict__ smooth,
+                                                                  const uint8_t* __restrict__ smooth_mask) {
+  using Acc = typename std::conditional<kSmooth, double, float>::type;
+  __shared__ Acc red[32];
+  __shared__ int isum[kThreads / 32];
+  // x / s_k for the 8 channels of vector i: s_k is read only for smoothed
+  // channels (mask bit set), the rest divide by 1.0 exactly (= x)
+  auto sdiv = [&](double xv, int64_t i, int t, uint32_t mbits) -> double {
+    if (smooth_mask == nullptr) return smooth_div(xv, smooth[i * 8 + t]);
+    return ((mbits >> t) & 1u) ? xv / smooth[i * 8 + t] : xv;
+  };
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t row = blockIdx.x;
+  const uint4* xv = reinterpret_cast<const uint4*>(x + row * ldx);
+  const int64_t nv = K / 8;  // 16-byte vectors in the row
+  uint4 v[kVPT];
+#pragma unroll
+  for (int j = 0; j < kVPT; ++j) {
+    const int64_t i = threadIdx.x + (int64_t)j * kThreads;
+    v[j] = i < nv ? __ldg(xv + i) : make_uint4(0, 0, 0, 0);
+  }
+  uint32_t mb[kVPT];
+#pragma unroll
+  for (int j = 0; j < kVPT; ++j) {
+    const int64_t i = threadIdx.x + (int64_t)j * kThreads;
+    mb[j] = (kSmooth && smooth_mask != nullptr && i < nv) ? (uint32_t)__ldg(smooth_mask + i) : 0u;
+  }
+  Acc m = Acc(0);
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < kVPT; ++j) {
+    const int64_t i = threadIdx.x + (int64_t)j * kThreads;
+    if (i < nv) {
+      const __half* e = reinterpret_cast<const __half*>(&v[j]);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        Acc a;
+        if constexpr (kSmooth) {
+          a = fabs(sdiv((double)__half2float(e[t]), i, t, mb[j]));
+        } else {
+          a = absval(e[t]);
+        }
+        bad |= is_bad(a);
+        m = a > m ? a : m;
+      }
+    }
+  }
+  if (__syncthreads_or(bad)) {
+    if (threadIdx.x == 0) atomicOr(status, kStatNonFinite);
+  }
+  m = block_max<kThreads, Acc>(m, red);
+  const double s = (m > Acc(0)) ? (double)m / 127.0 : 1.0;
+  if (threadIdx.x == 0) s_out[row] = s;
+  const bool zero_row = !(m > Acc(0));
+  const float inv = zero_row ? 0.0f : 127.0f / (float)m;
+  const double inv64 = 1.0 / s;
+  int8_t* qr = q + row * ldq;
+  int csum = 0;
+#pragma unroll
+  for (int j = 0; j < kVPT; ++j) {
+    const int64_t i = threadIdx.x + (int64_t)j * kThreads;
+    if (i < nv) {
+      const __half* e = reinterpret_cast<const __half*>(&v[j]);
+      alignas(8) int8_t out[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        int8_t c = 0;
+        if (!zero_row) {
+          if constexpr (kSmooth) {
+            c = quant_code_f64(sdiv((double)__half2float(e[t]), i, t, mb[j]), inv64, s);
+          } else {
+            c = quant_code_f16(__half2float(e[t]), inv, s);
+          }
+        }
+        out[t] = c;
+        csum += c;
+      }
+      *reinterpret_cast<uint2*>(qr + i * 8) = *reinterpret_cast<const uint2*>(out);
+    }
+  }
+  if (rowsum_out) {
+    for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+    if ((threadIdx.x & 31) == 0) isum[threadIdx.x >> 5] = csum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < kThreads / 32; ++w) t += isum[w];
+      rowsum_out[row] = t;
+    }
+  }
+}
+
 // rowsum of existing int8 codes (activations built outside quant_act_per_token)
 __global__ void rowsum_kernel(const int8_t* __restrict__ q, int64_t K, int64_t ldq, int32_t* __restrict__ out) {
   const int8_t* qr = q + (int64_t)blockIdx.x * ldq;
@@ -211,7 +330,8 @@ using namespace qqq;
 
 static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
                             double* s_a, int32_t* status_dev, const double* row_max_in, double* row_max_out,
-                            int32_t* rowsum, cudaStream_t stream, const double* smooth = nullptr) {
+                            int32_t* rowsum, cudaStream_t stream, const double* smooth = nullptr,
+                            const uint8_t* smooth_mask = nullptr) {
   if (M < 0 || K <= 0 || ldx < K || (!row_max_out && ldq < K)) return kErrShape;
   if (M == 0) return kOk;
   constexpr int kT = 256;
@@ -225,6 +345,20 @@ static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, in
   lc.attrs = attr;
   lc.numAttrs = 1;
   cudaError_t e;
+  // fp16 rows that fit one CTA's registers: the single-round-trip kernel
+  constexpr int kRT = 512, kRV = 4;
+  if (x_dtype == 0 && !row_max_in && !row_max_out && K % 8 == 0 &&
+      K <= (int64_t)kRT * kRV * 8 && ldx % 8 == 0 &&
+      ldq % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(q) & 7) == 0) {
+    lc.blockDim = dim3(kRT);
+    if (smooth)
+      e = cudaLaunchKernelEx(&lc, act_quant_row_kernel<kRT, kRV, true>, (const __half*)x, K, ldx, q, ldq, s_a,
+                             status_dev, rowsum, smooth, smooth_mask);
+    else
+      e = cudaLaunchKernelEx(&lc, act_quant_row_kernel<kRT, kRV, false>, (const __half*)x, K, ldx, q, ldq, s_a,
+                             status_dev, rowsum, smooth, smooth_mask);
+    return e == cudaSuccess ? kOk : kErrCuda;
+  }
   if (smooth) {
     if (row_max_in || row_max_out) return kErrConfig;
     switch (x_dtype) {
@@ -297,8 +431,9 @@ extern "C" int qqq_act_quant_with_max(const void* x, int x_dtype, int64_t M, int
 // apply_quant_linear's activation step (pipeline.py:146): quant_act_per_token
 // of x / s, the f64 division fused into the quantizer (one pass over x).
 extern "C" int qqq_act_quant_smooth(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx,
-                                    const double* smooth, int8_t* q, int64_t ldq, double* s_a, int32_t* rowsum,
-                                    int32_t* status_dev, cudaStream_t stream) {
+                                    const double* smooth, const uint8_t* smooth_mask, int8_t* q, int64_t ldq,
+                                    double* s_a, int32_t* rowsum, int32_t* status_dev, cudaStream_t stream) {
   if (!smooth) return kErrConfig;
-  return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, nullptr, nullptr, rowsum, stream, smooth);
+  return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, nullptr, nullptr, rowsum, stream, smooth,
+                          smooth_mask);
 }

@@ -22,7 +22,8 @@ import torch
 from . import _lib
 from .errors import ShapeError
 from .gemm import FusedScales, w4a8_gemm_per_channel, w4a8_gemm_per_group
-from .quantize import PER_CHANNEL, QuantizedActivations, QuantizedWeights, as_cuda, attach_rowsum, raise_if_bad
+from .quantize import (PER_CHANNEL, QuantizedActivations, QuantizedWeights, as_cuda, attach_rowsum, deferred_status,
+                       raise_if_bad)
 
 __all__ = ["SmoothingPlan", "QuantizedLayer", "identity_plan", "quant_act_smoothed", "apply_quant_linear"]
 
@@ -72,11 +73,14 @@ def quant_act_smoothed(x, s, check: bool = True) -> QuantizedActivations:
     qbuf = torch.empty((m, kp), dtype=torch.int8, device=dev)
     s_a = torch.empty((m,), dtype=torch.float64, device=dev)
     rowsum = torch.empty((m,), dtype=torch.int32, device=dev)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev) if check else deferred_status(dev)
     if m > 0:
         dt = {torch.float16: 0, torch.float32: 1, torch.float64: 2}[xt.dtype]
         ldx = xt.stride(0) if m > 1 else k
-        _lib.check(lib.qqq_act_quant_smooth(_lib.ptr(xt), dt, m, k, ldx, _lib.ptr(st), _lib.ptr(qbuf), kp,
+        # (no channel mask: with ~1/8 smoothed channels every warp diverges into the
+        # division anyway, and the mask loads measured slower)
+        _lib.check(lib.qqq_act_quant_smooth(_lib.ptr(xt), dt, m, k, ldx, _lib.ptr(st), None,
+                                            _lib.ptr(qbuf), kp,
                                             _lib.ptr(s_a), _lib.ptr(rowsum), _lib.ptr(status), _lib.stream_of(dev)),
                    "quant_act_smoothed")
     out = QuantizedActivations(q=qbuf[:, :k], s_a=s_a)

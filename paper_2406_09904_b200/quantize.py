@@ -64,6 +64,21 @@ def _status(device) -> torch.Tensor:
     return torch.zeros(1, dtype=torch.int32, device=device)
 
 
+_deferred: dict = {}
+
+
+def deferred_status(device) -> torch.Tensor:
+    """Per-device status word for asynchronous (check=False) calls: kernels only
+    OR error bits into it, so no per-call zero-fill launch breaks a PDL chain;
+    `raise_if_bad` on it raises and re-arms it."""
+    key = torch.device(device).index
+    st = _deferred.get(key)
+    if st is None:
+        st = torch.zeros(1, dtype=torch.int32, device=device)
+        _deferred[key] = st
+    return st
+
+
 @dataclass(frozen=True)
 class QuantSpec:
     """Weight/activation bit widths and weight quantization granularity (quantize.py:38-52)."""
@@ -134,7 +149,7 @@ def quant_act_per_token(x, check: bool = True) -> QuantizedActivations:
     qbuf = torch.empty((m, kp), dtype=torch.int8, device=dev)
     s_a = torch.empty((m,), dtype=torch.float64, device=dev)
     rowsum = torch.empty((m,), dtype=torch.int32, device=dev)
-    status = _status(dev)
+    status = _status(dev) if check else deferred_status(dev)
     if m > 0 and k > 0:
         dt = {torch.float16: 0, torch.float32: 1, torch.float64: 2}[xt.dtype]
         _lib.check(lib.qqq_act_quant_ex(_lib.ptr(xt), dt, m, k, ldx, _lib.ptr(qbuf), kp, _lib.ptr(s_a),
@@ -181,6 +196,8 @@ def rowsum_of(aq: QuantizedActivations) -> torch.Tensor:
 
 def raise_if_bad(status: torch.Tensor, what: str) -> None:
     v = int(status.item())
+    if v:
+        status.zero_()  # re-arm (matters for the shared deferred status word)
     if v & _lib.STAT_NONFINITE:
         raise DataError(f"{what} contains non-finite values")
     if v & _lib.STAT_CODE_RANGE:
