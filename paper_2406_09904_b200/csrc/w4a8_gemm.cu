@@ -758,7 +758,11 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
       }
       const bool owner = whole || seg_idx == 0;
       const int j = seg % C::kAccBufs;
+#ifdef QQQ_EPI_SLEEPWAIT
       mbar_wait_sleep(&acc_full[j], (seg / C::kAccBufs) & 1);
+#else
+      mbar_wait_backoff(&acc_full[j], (seg / C::kAccBufs) & 1);
+#endif
       tc_fence_after();
       if (lead && seg < 4) QQQ_STAMP(36 + 2 * seg);
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
