@@ -647,6 +647,21 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
               s1[i] = sv;
             }
           }
+          // Release the packed stage as soon as its bytes are in registers (before
+          // the conversion), so the producer refills it one conversion earlier:
+          // the asm consumes the last shared loads (LDS complete in order per
+          // warp), which makes every lane wait for its loads before the arrive.
+          {
+            uint32_t dep = v[kSlabs - 1].w;
+            if constexpr (MODE == kModePG) dep ^= s1[kSlabs - 1];
+            asm volatile("" ::"r"(dep));
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&w_empty[ws]);
+          if (++ws == C::kWStages) {
+            ws = 0;
+            wph ^= 1;
+          }
           uint32_t o[kSlabs][8];
 #pragma unroll
           for (int i = 0; i < kSlabs; ++i) {
@@ -668,13 +683,6 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
               pg_convert_word<false, true>(v[i].z, s2, s16, magic, o[i][4], o[i][5]);
               pg_convert_word<false, true>(v[i].w, s2, s16, magic, o[i][6], o[i][7]);
             }
-          }
-          // the packed stage is consumed (the converted values are in registers): release it
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&w_empty[ws]);
-          if (++ws == C::kWStages) {
-            ws = 0;
-            wph ^= 1;
           }
           conv_wait(&kb_empty[ab], aph ^ 1);
           tc_fence_after();
