@@ -75,14 +75,14 @@ struct Cfg {
   static constexpr bool kSmall = NTOK <= 64 && MODE != kModeI8;  // (I8 stages are 2x larger)
   static constexpr int kCtasPerSm = kSmall ? 2 : 1;
 #ifndef QQQ_BIG_CONV_WARPS
-#define QQQ_BIG_CONV_WARPS 16
+#define QQQ_BIG_CONV_WARPS 8
 #endif
   // 2 per TMEM lane quadrant: each converter warp handles >= 2 slabs per
   // k-block so the per-k-block handshake cost (~80 instructions per warp) stays
   // well below the conversion work
   static constexpr int kNumConvWarps = kSmall ? 8 : QQQ_BIG_CONV_WARPS;
 #ifndef QQQ_BIG_EPI_WARPS
-#define QQQ_BIG_EPI_WARPS 8
+#define QQQ_BIG_EPI_WARPS 12
 #endif
   static constexpr int kNumEpiWarps = kSmall ? 4 : QQQ_BIG_EPI_WARPS;  // groups of 4 (one warp per lane quadrant)
   static constexpr int kEpiGroups = kNumEpiWarps / 4;
@@ -97,7 +97,9 @@ struct Cfg {
   static constexpr int kNumThreads = ((kSmall ? kWProducerWarp : kMmaWarp) + 1) * 32;
   static constexpr int kSmemBudget = kSmall ? 111 * 1024 : 225 * 1024;
   static constexpr int kTmemBudget = kSmall ? 256 : 512;
-  static constexpr int kEpiSmem = kNumEpiWarps * 2048 + kEpiGroups * 2 * 8192;  // y staging + split-K partial ring
+  // split-K partial ring depth per epilogue group (2 when the shared memory allows)
+  static constexpr int kPartBufs = kEpiGroups > 2 ? 1 : 2;
+  static constexpr int kEpiSmem = kNumEpiWarps * 2048 + kEpiGroups * kPartBufs * 8192;  // y staging + partial ring
   // Two rings. Weights: their own TMA ring (released by the converters once
   // the packed bytes are consumed, or by the MMA in I8 mode). K-blocks: ring
   // slot s = activation stage s = TMEM A buffer s, guarded by ONE full barrier
@@ -133,8 +135,8 @@ struct Cfg {
   static constexpr int kOffSA = kOffBar + (kNumBars * 8 + 16 + 15) / 16 * 16;  // per-token scales of a tile (f64)
   static constexpr int kOffRS = kOffSA + NTOK * 8;                             // per-token code sums (int32)
   static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;  // per epilogue warp: 2 x [16 tok][32 ch] fp16
-  static constexpr int kOffPart = kOffY + kNumEpiWarps * 2048;         // per group: 2 x 8 KiB split-K partial chunks
-  static constexpr int kSmemBytes = kOffPart + kEpiGroups * 2 * 8192 + 1024;  // +1024 alignment slack
+  static constexpr int kOffPart = kOffY + kNumEpiWarps * 2048;  // per group: kPartBufs x 8 KiB split-K partial chunks
+  static constexpr int kSmemBytes = kOffPart + kEpiGroups * kPartBufs * 8192 + 1024;  // +1024 alignment slack
   static_assert(kSmemBytes <= kSmemBudget + 1024 && kSmemBytes * kCtasPerSm <= 227 * 1024,
                 "over the per-CTA shared memory budget");
   static constexpr int kTmemNeed = kAccCols + kABufs * kACols;
@@ -731,7 +733,8 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
     double* sa_smem = reinterpret_cast<double*>(smem + C::kOffSA);
     int32_t* rs_smem = reinterpret_cast<int32_t*>(smem + C::kOffRS);
     uint8_t* ystage = smem + C::kOffY + (warp - C::kEpiWarp0) * 2048;  // per warp: 2 x [16 tok][32 ch] fp16
-    uint8_t* pstage = smem + C::kOffPart + eh * 16384;
+    constexpr int PB = C::kPartBufs;
+    uint8_t* pstage = smem + C::kOffPart + eh * (PB * 8192);
     uint64_t* pfull = part_full + 2 * eh;
     uint32_t ych = 0;     // y staging chunks issued by this half
     uint32_t pchunk = 0;  // partial-sum chunks consumed by this half (part_full parity)
@@ -793,8 +796,8 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
               if (c0 + i < tvalid) red_add_s32(slots + (c0 + i) * 128 + row, (int32_t)r[i]);
           } else {
             // rows past tvalid hold zeros (their activations were zero-filled)
-            int32_t* stg = reinterpret_cast<int32_t*>(pstage + (pcon & 1) * 8192);
-            if (hlead) bulk_wait_read<1>();  // the reduce that used this buffer two chunks ago has read it
+            int32_t* stg = reinterpret_cast<int32_t*>(pstage + (pcon % PB) * 8192);
+            if (hlead) bulk_wait_read<PB - 1>();  // the reduce that used this buffer PB chunks ago has read it
             named_bar_sync(kBarHalf, kHalf);
 #pragma unroll
             for (int i = 0; i < 16; ++i) stg[i * 128 + row] = (int32_t)r[i];
@@ -838,13 +841,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
         // slot) are bulk-copied into this half's 2-deep smem ring, one chunk ahead
         auto part_issue = [&](int li) {
           const uint32_t pc = pchunk + li;
-          mbar_arrive_expect_tx(&pfull[pc & 1], 8192);
-          bulk_g2s(pstage + (pc & 1) * 8192, slots + (int64_t)(eh + H * li) * 16 * 128, 8192, &pfull[pc & 1]);
+          mbar_arrive_expect_tx(&pfull[pc % PB], 8192);
+          bulk_g2s(pstage + (pc % PB) * 8192, slots + (int64_t)(eh + H * li) * 16 * 128, 8192, &pfull[pc % PB]);
         };
         if (!whole && hlead) {
           bulk_wait_read<0>();  // earlier contributor reductions have read the shared ring
-          if (nmine > 0) part_issue(0);
-          if (nmine > 1) part_issue(1);
+          for (int li = 0; li < PB && li < nmine; ++li) part_issue(li);
         }
 #pragma unroll 1
         for (int li = 0; li < nmine; ++li) {
@@ -855,9 +857,9 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
           if (lead && seg == 0 && li < 16) QQQ_STAMP(44 + li);
           if (!whole) {
             const uint32_t pc = pchunk + li;
-            mbar_wait(&pfull[pc & 1], (pc >> 1) & 1);
+            mbar_wait(&pfull[pc % PB], (pc / PB) & 1);
             if (lead && li == 0) QQQ_STAMP(62);
-            const int32_t* part = reinterpret_cast<const int32_t*>(pstage + (pc & 1) * 8192);
+            const int32_t* part = reinterpret_cast<const int32_t*>(pstage + (pc % PB) * 8192);
 #pragma unroll
             for (int i = 0; i < 16; ++i) r[i] += (uint32_t)part[i * 128 + row];
             // return the slot to zero for the next launch (entries past tvalid were never touched)
@@ -865,7 +867,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
             for (int i = 0; i < 16; ++i)
               if (c0 + i < tvalid) __stcg(slots + (c0 + i) * 128 + row, 0);
             named_bar_sync(kBarHalf, kHalf);  // this half has read the buffer
-            if (hlead && li + 2 < nmine) part_issue(li + 2);
+            if (hlead && li + PB < nmine) part_issue(li + PB);
           }
           if constexpr (C::kU8) {
 #pragma unroll
@@ -1003,13 +1005,13 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
 
 // Tile-plan cost model (us), fitted (log least squares, scripts/fit_planner.py)
 // to the B200 tile-plan sweep profiles/r01_tileplan_sweep_v2.jsonl of this
-// kernel (0.8% regret against the best measured plan over the C2 sweep):
+// kernel (0.9% regret against the best measured plan over the C2 sweep):
 //   per-k-block time u = max(weight bytes / per-CTA HBM share, conversion, MMA)
 //   whole tiles: T = T0 + units_per_CTA * u + waves * epilogue
 //   stream-K:    T = T0 + units_per_CTA * u + fix-up + epilogue
 static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
-  const double T0 = 1.801, kBsm = 499.9e3, kBtot = 6382e3, kConv = 14.62e-6, kMma = 1.495, kF0 = 1.643,
-               kF1 = 0.6073, kE0 = 3.077, kE1 = 0.004508;
+  const double T0 = 1.714, kBsm = 218.7e3, kBtot = 11640e3, kConv = 14.36e-6, kMma = 1.461, kF0 = 1.87,
+               kF1 = 0.5761, kE0 = 3.524, kE1 = 0.004834;
   const double clk = 1900.0;  // MHz
   const int cps = lp.ntok <= 64 ? 2 : 1;
   const int64_t ucta = lp.aligned_tiles > 0 ? (int64_t)lp.aligned_tiles * lp.kb_per_tile
