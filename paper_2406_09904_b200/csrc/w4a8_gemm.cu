@@ -98,7 +98,8 @@ struct Cfg {
   static constexpr int kSmemBudget = kSmall ? 111 * 1024 : 225 * 1024;
   static constexpr int kTmemBudget = kSmall ? 256 : 512;
   // split-K partial ring depth per epilogue group (2 when the shared memory allows)
-  static constexpr int kPartBufs = kEpiGroups > 2 ? 1 : 2;
+  // (the NTOK=256 prefill tiles, mostly whole tiles, give it up for activation stages)
+  static constexpr int kPartBufs = (kEpiGroups > 2 && NTOK >= 256) ? 1 : 2;
   static constexpr int kEpiSmem = kNumEpiWarps * 2048 + kEpiGroups * kPartBufs * 8192;  // y staging + partial ring
   // Two rings. Weights: their own TMA ring (released by the converters once
   // the packed bytes are consumed, or by the MMA in I8 mode). K-blocks: ring
@@ -1036,8 +1037,11 @@ static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force
   }
   LaunchPlan best{};
   double best_t = 1e30;
-  for (int nt : {16, 32, 64, 128, 256}) {
-    if (nt > 16 && nt / 2 >= M) break;  // a smaller tile already covers every token
+  // NTOK=64 stays available by config but is not auto-selected: as a half-SM
+  // CTA it only fits 2 weight + 2 activation stages, and the NTOK=128 plan
+  // measured faster at every M it would cover (r01_tileplan_sweep_v2)
+  for (int nt : {16, 32, 128, 256}) {
+    if (nt > 32 && nt / 4 >= M) break;  // a smaller tile already covers every token
     for (int sk = 0; sk < 2; ++sk) {  // whole tiles / stream-K (the hybrid never won a sweep point)
       const LaunchPlan lp = plan_for(mode, M, N, K, nt, sk, 0);
       if (lp.tiles > 65536) continue;
