@@ -109,6 +109,7 @@ QQQ_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
 QQQ_DEVICE void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
+  unsigned long long t0 = 0;
 #pragma unroll 1
   for (uint32_t n = 0;; ++n) {
     asm volatile(
@@ -120,9 +121,64 @@ QQQ_DEVICE void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
         : "memory");
     if (done) return;
 #ifndef QQQ_NO_WATCHDOG
-    if (n > (1u << 22)) __trap();
+    // a suspended poll may last up to the hint: bound the wait in time (~4 s)
+    if ((n & 255) == 255) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) __trap();
+    }
 #endif
   }
+}
+
+// ---- 2-CTA cluster (cta_group::2) helpers ----
+QQQ_DEVICE uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of `p` (a shared::cta variable) in CTA `rank` of the cluster
+QQQ_DEVICE uint32_t mapa_shared(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// Arrive on a barrier of another CTA of the cluster. Default (.release.cta)
+// semantics: a .cluster-scope release compiles to MEMBAR.ALL.GPU, which under a
+// streaming HBM load costs ~0.9 us per arrive (measured); the data it guards
+// is tcgen05/async-proxy traffic, ordered by the tcgen05 fences and the
+// mbarrier itself.
+QQQ_DEVICE void mbar_arrive_cluster(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+}
+// parity wait with cluster-scope acquire (arrivals come from the peer CTA too)
+QQQ_DEVICE void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  unsigned long long t0 = 0;
+#pragma unroll 1
+  for (uint32_t n = 0;; ++n) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity), "r"(0x100000u)
+        : "memory");
+    if (done) return;
+#ifndef QQQ_NO_WATCHDOG
+    if ((n & 255) == 255) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) __trap();
+    }
+#endif
+  }
+}
+QQQ_DEVICE void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // Parity wait for a role that idles for most of the kernel (the epilogue
@@ -190,6 +246,37 @@ QQQ_DEVICE void tmem_alloc(uint32_t* smem_result, uint32_t ncols) {
 
 QQQ_DEVICE void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// pair (cta_group::2) TMEM allocation: the warp with the same id in both CTAs
+// of the pair executes it; both CTAs get the same column range
+QQQ_DEVICE void tmem_alloc_pair(uint32_t* smem_result, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_result)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+QQQ_DEVICE void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// pair MMA (issued by the even CTA): D (M = 256 rows, 128 per CTA's TMEM) (+)=
+// A[tmem, 128 rows per CTA] * B[smem, N/2 rows per CTA]^T
+QQQ_DEVICE void mma_i8_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit of the pair's MMAs, arriving on the barrier at the same offset in every CTA of `mask`
+QQQ_DEVICE void mma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 
 QQQ_DEVICE void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }

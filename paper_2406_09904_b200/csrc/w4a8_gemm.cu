@@ -61,12 +61,21 @@ struct GemmParams {
   int dp_tiles;             // hybrid: CTA b first owns whole tiles [b*dp_tiles, (b+1)*dp_tiles), then
   int64_t sk_unit0;         //   its stream-K share of the units [sk_unit0, sk_unit0 + units)
   int y_tma;                // 1: y written by TMA stores from a shared-memory staging tile
+  int pair;                 // 1: 2-CTA clusters (cta_group::2); tiles count 256-channel pair tiles
   unsigned long long* dbg;  // optional per-CTA %globaltimer timeline, diagnostics only
 };
 
-template <int MODE, int NTOK, int BK>
+template <int MODE, int NTOK, int BK, bool PAIR = false>
 struct Cfg {
   static constexpr bool kConvert = MODE != kModeI8;
+  // PAIR: a 2-CTA cluster computes a 256-channel x NTOK tile with
+  // tcgen05.mma.cta_group::2 (UMMA M=256): each CTA converts its own 128
+  // channels into its own TMEM, but loads only HALF of the activation tile
+  // (NTOK/2 tokens; the pair's MMA reads B from both CTAs' shared memory), so
+  // the per-SM activation traffic and staging halve — the NTOK=256 prefill
+  // tile is otherwise starved of activation + weight bytes in flight.
+  static constexpr bool kPair = PAIR;
+  static constexpr int kTokLoad = PAIR ? NTOK / 2 : NTOK;  // activation rows this CTA loads per k-block
   // ---- CTA shape. Decode/mid tiles (NTOK <= 64) use a half-SM CTA: two per SM,
   // so a CTA's prologue / first-byte latency / epilogue tail overlaps the other
   // CTA's stream, and under PDL the next kernel's CTAs start (and prefetch
@@ -81,6 +90,16 @@ struct Cfg {
   // k-block so the per-k-block handshake cost (~80 instructions per warp) stays
   // well below the conversion work
   static constexpr int kNumConvWarps = kSmall ? 8 : QQQ_BIG_CONV_WARPS;
+#ifndef QQQ_PAIR_CONV_GROUPS
+#define QQQ_PAIR_CONV_GROUPS 2
+#endif
+  // k-block interleaving: converter group g (kNumConvWarps / kConvGroups warps,
+  // covering all 128 rows and BK of k) takes the k-blocks it with it % groups ==
+  // g, so each warp's fixed per-k-block latency (barrier waits, TMEM store
+  // completion, arrive) overlaps the other group's k-block
+  static constexpr int kConvGroups = PAIR ? QQQ_PAIR_CONV_GROUPS : 1;
+  static constexpr int kConvPerGroup = kNumConvWarps / kConvGroups;
+  static_assert(kConvPerGroup % 4 == 0, "a converter group covers the 4 TMEM lane quadrants");
 #ifndef QQQ_BIG_EPI_WARPS
 #define QQQ_BIG_EPI_WARPS 12
 #endif
@@ -107,7 +126,7 @@ struct Cfg {
   // (activation TMA bytes + one arrival per converter warp + the producer's
   // arrive) and ONE empty barrier (the MMA's commit), so the MMA warp pays one
   // wait and one commit per k-block (each ~130 cycles, scripts/mma_probe2.cu).
-  static constexpr int kXBytes = NTOK * BK;
+  static constexpr int kXBytes = kTokLoad * BK;
   static constexpr int kSSMax = MODE == kModeI8 ? 16384 : MODE == kModePC ? 8192 : 8192 + 256 * 4;
   static constexpr int kWBytes = (BK / 128) * kSSMax;  // worst case (PG, g = 32)
   // Converted int8 weights (the MMA A operand) live in TMEM, not shared memory:
@@ -122,7 +141,8 @@ struct Cfg {
   // k-block ring depth: what is left after 3 weight stages, at most 4 and at
   // most the number of TMEM A buffers that fit beside the accumulators
   static constexpr int kXStagesRaw = (kRingBudget - 3 * kWBytes) / kXBytes;
-  static constexpr int kXCap = kABufsMax < 4 ? kABufsMax : 4;
+  static constexpr int kXCapWanted = PAIR ? 6 : 4;
+  static constexpr int kXCap = kABufsMax < kXCapWanted ? kABufsMax : kXCapWanted;
   static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > kXCap ? kXCap : kXStagesRaw);
   static constexpr int kABufs = kConvert ? kXStages : 0;
   static constexpr int kWStagesRaw = (kRingBudget - kXStages * kXBytes) / kWBytes;
@@ -147,7 +167,7 @@ struct Cfg {
   // per-group: the converter emits w8 + 128 (no XOR); the MMA runs u8 x s8 and
   // the epilogue subtracts 128 * rowsum(a) — exact in int32 (K <= 65536)
   static constexpr bool kU8 = MODE == kModePG;
-  static constexpr uint32_t kIdesc = make_idesc_i8(128, NTOK, kU8);
+  static constexpr uint32_t kIdesc = make_idesc_i8(PAIR ? 256 : 128, NTOK, kU8);
   static_assert(NTOK % 16 == 0 && NTOK >= 16 && NTOK <= 256, "invalid UMMA N");
   static_assert(BK % 128 == 0, "BK must be a multiple of the 128-byte swizzle atom");
 };
@@ -198,6 +218,18 @@ QQQ_DEVICE __half f64_to_f16_rn(double v) {
 
 QQQ_DEVICE void red_add_s32(int32_t* p, int32_t v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// pair mode: this CTA's half of the activation tile lands in its own shared
+// memory; the transaction bytes complete on the EVEN CTA's barrier (cl_bar, a
+// shared::cluster address), which the pair MMA issuer waits on
+QQQ_DEVICE void tma_load_3d_pair(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
+                                 uint32_t cl_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(cl_bar)
+      : "memory");
 }
 
 QQQ_DEVICE void tma_load_3d(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
@@ -303,8 +335,9 @@ QQQ_DEVICE SegIter make_iter(const GemmParams& p) {
   it.kbt = p.kb_per_tile;
   it.v = it.v1 = 0;
   if (p.aligned_tiles > 0) {
-    const int64_t tiles = (int64_t)p.n_tiles * p.tok_tiles;
-    int64_t t0 = (int64_t)blockIdx.x * p.aligned_tiles;
+    // pair plans: the CTA pair (2b, 2b+1) owns 256-channel pair tiles
+    const int64_t tiles = (int64_t)(p.pair ? (p.n_tiles + 1) / 2 : p.n_tiles) * p.tok_tiles;
+    int64_t t0 = (int64_t)(p.pair ? blockIdx.x >> 1 : blockIdx.x) * p.aligned_tiles;
     int64_t t1 = t0 + p.aligned_tiles < tiles ? t0 + p.aligned_tiles : tiles;
     if (t0 > tiles) t0 = tiles;
     if (t1 < t0) t1 = t0;
@@ -362,11 +395,12 @@ QQQ_DEVICE void issue_weight_kblock(const GemmParams& p, const UnitCursor& c, ui
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <int MODE, int NTOK, int BK>
-__global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NTOK, BK>::kCtasPerSm)
+template <int MODE, int NTOK, int BK, bool PAIR>
+__global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MODE, NTOK, BK, PAIR>::kCtasPerSm)
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap y_map,
                      const GemmParams p) {
-  using C = Cfg<MODE, NTOK, BK>;
+  using C = Cfg<MODE, NTOK, BK, PAIR>;
+  static_assert(!PAIR || (C::kConvert && !C::kSmall && C::kAccBufs == 1), "pair mode: prefill convert tiles");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
@@ -381,29 +415,43 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // Pair mode: CTA rank 0 of the cluster ("even" CTA) issues the pair MMAs and
+  // owns the barriers they wait on (k-block full: both CTAs' activation bytes
+  // and converter arrivals; accumulator empty: both CTAs' epilogues); the
+  // MMA commits arrive on the barrier copies of both CTAs.
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+  // output-channel tile of a (pair) tile index
+  auto ntile_of = [&](int tile) -> int {
+    return PAIR ? (tile / p.tok_tiles) * 2 + (int)crank : tile / p.tok_tiles;
+  };
 
   if (threadIdx.x == 0) {
     QQQ_STAMP(0);
     griddep_launch_dependents();
     for (int s = 0; s < C::kXStages; ++s) {
-      mbar_init(&kb_full[s], C::kConvert ? C::kNumConvWarps + 1 : 1);
+      mbar_init(&kb_full[s], C::kConvert ? (PAIR ? 2 : 1) * C::kConvPerGroup + 1 : 1);
       mbar_init(&kb_empty[s], 1);
     }
     if (!C::kSmall) {  // small CTAs: the producer warp owns (and initialises) its weight ring
       for (int s = 0; s < C::kWStages; ++s) {
         mbar_init(&w_full[s], 1);
-        mbar_init(&w_empty[s], C::kConvert ? C::kNumConvWarps : 1);
+        mbar_init(&w_empty[s], C::kConvert ? C::kConvPerGroup : 1);
       }
     }
     for (int j = 0; j < C::kAccBufs; ++j) {
       mbar_init(&acc_full[j], 1);
-      mbar_init(&acc_empty[j], C::kNumEpiWarps);
+      mbar_init(&acc_empty[j], (PAIR ? 2 : 1) * C::kNumEpiWarps);
     }
     for (int i = 0; i < 2 * C::kEpiGroups; ++i) mbar_init(&part_full[i], 1);
     mbar_fence_init();
   }
   if (warp == C::kActProducerWarp && lane == 0) tma_prefetch_desc(&act_map);
-  if (warp == C::kAllocWarp) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == C::kAllocWarp) {
+    if constexpr (PAIR)
+      tmem_alloc_pair(tmem_slot, C::kTmemCols);
+    else
+      tmem_alloc(tmem_slot, C::kTmemCols);
+  }
   if (C::kSmall && warp == C::kWProducerWarp) {
     // The first weight copies do not wait for the CTA set-up (TMEM allocation,
     // other barriers): the decode critical path starts with this HBM latency.
@@ -425,9 +473,15 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive / TMA signal
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // the even CTA's k-block-full and accumulator-empty barriers (pair mode)
+  const uint32_t kb_full_cl = PAIR ? mapa_shared(kb_full, 0) : 0u;
+  const uint32_t acc_empty_cl = PAIR ? mapa_shared(acc_empty, 0) : 0u;
 
   // The single-issuer roles (producers, MMA) run their loops with the whole
   // warp converged and elect one lane per async instruction: the operands are
@@ -497,7 +551,9 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
     int tile, kb0, kb1;
     uint32_t s = 0, ph = 0;
     while (si.next(tile, kb0, kb1)) {
-      const int n_tile = tile / p.tok_tiles;
+      // (pair mode, odd channel-tile count: the missing last tile converts a copy of
+      //  a real one; its rows are never stored)
+      const int n_tile = min(ntile_of(tile), p.n_tiles - 1);
 #pragma unroll 1
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait_sleep(&w_empty[s], ph ^ 1);
@@ -531,12 +587,19 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait_sleep(&kb_empty[s], ph ^ 1);
         if (elect_one()) {
+          if constexpr (PAIR) {
+            // each CTA loads its half of the tokens; the bytes of both count on the even CTA's barrier
+            if (crank == 0) mbar_arrive_expect_tx(&kb_full[s], 2 * C::kXBytes);
+            tma_load_3d_pair(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0 + (int)crank * C::kTokLoad,
+                             kb * (BK / 128), kb_full_cl + s * 8);
+          } else {
 #ifdef QQQ_EXP_HALF_X
-          mbar_arrive_expect_tx(&kb_full[s], NTOK >= 128 ? C::kXBytes / 2 : C::kXBytes);
+            mbar_arrive_expect_tx(&kb_full[s], NTOK >= 128 ? C::kXBytes / 2 : C::kXBytes);
 #else
-          mbar_arrive_expect_tx(&kb_full[s], C::kXBytes);
+            mbar_arrive_expect_tx(&kb_full[s], C::kXBytes);
 #endif
-          tma_load_3d(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0, kb * (BK / 128), &kb_full[s]);
+            tma_load_3d(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0, kb * (BK / 128), &kb_full[s]);
+          }
         }
         __syncwarp();
         if (++s == C::kXStages) {
@@ -545,19 +608,26 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
         }
       }
     }
-  } else if (warp == C::kMmaWarp) {
+  } else if (warp == C::kMmaWarp && crank == 0) {
     // ============================ MMA issuer ============================
+    // (pair mode: the even CTA issues for both; the odd CTA's MMA warp idles)
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
     uint32_t it = 0, seg = 0;
     uint32_t xs = 0, xph = 0, ws = 0, wph = 0, j = 0, jph = 0;
     while (si.next(tile, kb0, kb1)) {
-      mbar_wait_sleep(&acc_empty[j], jph ^ 1);
+      if constexpr (PAIR)
+        mbar_wait_cluster(&acc_empty[j], jph ^ 1);
+      else
+        mbar_wait_sleep(&acc_empty[j], jph ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + j * NTOK;
 #pragma unroll 1
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
-        mma_wait(&kb_full[xs], xph);  // activations landed and (convert modes) the A buffer is converted
+        if constexpr (PAIR)
+          mbar_wait_cluster(&kb_full[xs], xph);
+        else
+          mma_wait(&kb_full[xs], xph);  // activations landed and (convert modes) the A buffer is converted
         if (lane == 0 && it < 16) QQQ_STAMP(96 + it);
         if constexpr (!C::kConvert) mma_wait(&w_full[ws], wph);
         tc_fence_after();
@@ -570,16 +640,21 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
 #pragma unroll
           for (int kk = 0; kk < BK / 32; ++kk) {
             // B: SWIZZLE_128B [k-atom][NTOK rows][128 B]; 32 B K-steps inside the atom
-            const uint64_t b_desc = b_desc0 + (uint64_t)(((kk / 4) * (NTOK * 128) + (kk % 4) * 32) >> 4);
+            const uint64_t b_desc = b_desc0 + (uint64_t)(((kk / 4) * (C::kTokLoad * 128) + (kk % 4) * 32) >> 4);
             const uint32_t acc = kk > 0 ? 1u : acc0;
-            if constexpr (C::kConvert) {
+            if constexpr (PAIR) {
+              mma_i8_ts_pair(d_tmem, a_tmem + kk * 8, b_desc, C::kIdesc, acc);
+            } else if constexpr (C::kConvert) {
               mma_i8_ts(d_tmem, a_tmem + kk * 8, b_desc, C::kIdesc, acc);  // A: 8 TMEM columns per K=32
             } else {
               // A: canonical K-major, no swizzle: [k16 chunk][128 rows][16 B]
               mma_i8_ss(d_tmem, make_smem_desc(a_smem + kk * 2 * 2048, 2048, 128, 0), b_desc, C::kIdesc, acc);
             }
           }
-          mma_commit(&kb_empty[xs]);
+          if constexpr (PAIR)
+            mma_commit_pair(&kb_empty[xs], 0x3);
+          else
+            mma_commit(&kb_empty[xs]);
           if constexpr (!C::kConvert) mma_commit(&w_empty[ws]);
         }
         __syncwarp();
@@ -595,7 +670,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
           }
         }
       }
-      if (elect_one()) mma_commit(&acc_full[j]);
+      if (elect_one()) {
+        if constexpr (PAIR)
+          mma_commit_pair(&acc_full[j], 0x3);
+        else
+          mma_commit(&acc_full[j]);
+      }
       __syncwarp();
       if (++j == C::kAccBufs) {
         j = 0;
@@ -608,9 +688,11 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
     // Warp w owns TMEM lane quadrant q = w % 4 (rows 32q..32q+31) and every
     // other 32-k slab (parity w / 4): thread = one output channel.
     if constexpr (C::kConvert) {
-      const int q = warp & 3, h = warp >> 2;  // quadrant, slab phase (0..kPhases-1)
+      constexpr int kPhases = C::kConvPerGroup / 4;
+      const int q = warp & 3, h = (warp >> 2) % kPhases;  // quadrant, slab phase (0..kPhases-1)
+      const int grp = (warp >> 2) / kPhases;               // k-block interleaving group
+      const bool stamp_warp = warp % C::kConvPerGroup == 0;
       const int row = q * 32 + lane;
-      constexpr int kPhases = C::kNumConvWarps / 4;
       constexpr int kSlabs = BK / 32 / kPhases;  // slabs per warp per k-block
       uint32_t magic;
       asm("mov.b32 %0, 0x64006400;" : "=r"(magic));  // a register operand for the fused and-or lop3
@@ -634,8 +716,19 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
       while (si.next(tile, kb0, kb1)) {
 #pragma unroll 1
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          if (C::kConvGroups > 1 && (int)(it % C::kConvGroups) != grp) {  // the other group's k-block
+            if (++ws == C::kWStages) {
+              ws = 0;
+              wph ^= 1;
+            }
+            if (++ab == C::kABufs) {
+              ab = 0;
+              aph ^= 1;
+            }
+            continue;
+          }
           conv_wait(&w_full[ws], wph);
-          if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(4 + it);
+          if (stamp_warp && lane == 0 && it < 16) QQQ_STAMP(4 + it);
           const uint32_t wst = wst0 + ws * C::kWBytes;
           uint4 v[kSlabs];
           uint32_t s1[kSlabs];
@@ -689,7 +782,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
           }
           conv_wait(&kb_empty[ab], aph ^ 1);
           tc_fence_after();
-          if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(64 + it);
+          if (stamp_warp && lane == 0 && it < 16) QQQ_STAMP(64 + it);
           const uint32_t abase = a_lane + ab * C::kACols;
 #ifndef QQQ_EXP_NO_STTM
 #pragma unroll
@@ -700,12 +793,17 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
 #endif
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&kb_full[ab]);
+          if (lane == 0) {
+            if constexpr (PAIR)
+              mbar_arrive_cluster(kb_full_cl + ab * 8);
+            else
+              mbar_arrive(&kb_full[ab]);
+          }
           if (++ab == C::kABufs) {
             ab = 0;
             aph ^= 1;
           }
-          if (warp == 0 && lane == 0 && it < 16) QQQ_STAMP(80 + it);
+          if (stamp_warp && lane == 0 && it < 16) QQQ_STAMP(80 + it);
         }
       }
     }
@@ -744,7 +842,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
     int tile, kb0, kb1;
     uint32_t seg = 0;
     while (si.next(tile, kb0, kb1)) {
-      const int n_tile = tile / p.tok_tiles;
+      const int n_tile = ntile_of(tile);
       const int tok0 = (tile % p.tok_tiles) * NTOK;
       const int tvalid = (p.M - tok0) < NTOK ? (p.M - tok0) : NTOK;
       // stage this tile's per-token scales (and code sums) while the MMAs run
@@ -875,7 +973,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
             for (int i = 0; i < 16; ++i) r[i] -= (uint32_t)rs_smem[c0 + i];  // u8 weights carried +128
           }
           store_outputs(p, r, sa_smem + c0, tok0 + c0, tvalid - c0, n, n_ok, s_col);
-          if (p.y_tma) {
+          if (p.y_tma && (!PAIR || n_tile < p.n_tiles)) {
             // y chunk -> this warp's staging [16 tok][32 ch] fp16 -> its own TMA store
             // (OOB rows/cols clipped): no cross-warp barrier on the store path
             uint16_t* stg = reinterpret_cast<uint16_t*>(ystage) + (ych & 1) * 512;
@@ -896,7 +994,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[j]);
+        if (lane == 0) {
+          if constexpr (PAIR)
+            mbar_arrive_cluster(acc_empty_cl + j * 8);
+          else
+            mbar_arrive(&acc_empty[j]);
+        }
         if (!whole) pchunk += nmine;
       }
       if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
@@ -906,10 +1009,20 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK>::kNumThreads, Cfg<MODE, NT
     if (lead) QQQ_STAMP(63);
   }
 
-  __syncthreads();
+  if constexpr (PAIR) {
+    // no CTA of the pair retires while the other may still signal its barriers
+    // or the pair MMAs may still read its shared memory / TMEM
+    tc_fence_before();
+    cluster_sync_all();
+  } else {
+    __syncthreads();
+  }
   if (warp == C::kAllocWarp) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::kTmemCols);
+    if constexpr (PAIR)
+      tmem_dealloc_pair(tmem_base, C::kTmemCols);
+    else
+      tmem_dealloc(tmem_base, C::kTmemCols);
   }
 }
 
@@ -945,7 +1058,7 @@ static int num_sms() {
 }
 
 struct LaunchPlan {
-  int ntok, bk, grid, aligned_tiles, tok_tiles, n_tiles, kb_per_tile, tiles, max_segs, dp_tiles;
+  int ntok, bk, grid, aligned_tiles, tok_tiles, n_tiles, kb_per_tile, tiles, max_segs, dp_tiles, pair;
   int64_t units, sk_unit0;
 };
 
@@ -957,11 +1070,33 @@ struct LaunchPlan {
 #endif
 static constexpr int bk_for(int mode, int ntok) { return ntok <= 64 ? 256 : mode == kModeI8 ? 128 : QQQ_BIG_BK; }
 static constexpr int ctas_per_sm(int mode, int ntok) { return ntok <= 64 && mode != kModeI8 ? 2 : 1; }
+#ifndef QQQ_PAIR_BK
+#define QQQ_PAIR_BK 128
+#endif
+static constexpr int kPairBk = QQQ_PAIR_BK;
 
 // split: 0 = whole tiles (data-parallel), 1 = stream-K over all units,
-//        2 = hybrid: full waves of whole tiles, the remainder stream-K'd over all CTAs
+//        2 = hybrid: full waves of whole tiles, the remainder stream-K'd over all CTAs,
+//        3 = whole 256-channel pair tiles on 2-CTA clusters (NTOK = 256, PC/PG)
 static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, int split, int force_grid) {
   LaunchPlan lp{};
+  if (split == 3 && (ntok != 256 || mode == kModeI8)) split = 0;
+  if (split == 3) {
+    lp.ntok = ntok;
+    lp.bk = kPairBk;
+    lp.pair = 1;
+    lp.tok_tiles = (int)((M + ntok - 1) / ntok);
+    lp.n_tiles = (int)(round_up(N, kTileN) / kTileN);
+    lp.kb_per_tile = (int)((round_up(K, kKPadTo) + lp.bk - 1) / lp.bk);
+    lp.tiles = ((lp.n_tiles + 1) / 2) * lp.tok_tiles;  // pair tiles
+    lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
+    lp.max_segs = 1;
+    const int pairs = (force_grid > 0 ? std::min(force_grid, num_sms()) : num_sms()) / 2;
+    const int per = (lp.tiles + pairs - 1) / pairs;
+    lp.aligned_tiles = per;
+    lp.grid = 2 * ((lp.tiles + per - 1) / per);
+    return lp;
+  }
   lp.ntok = ntok;
   lp.bk = bk_for(mode, ntok);
   lp.tok_tiles = (int)((M + ntok - 1) / ntok);
@@ -1065,11 +1200,11 @@ static size_t plan_ws_bytes(const LaunchPlan& lp) {
   return kCounterBytes + (size_t)lp.tiles * lp.ntok * 128 * 4;
 }
 
-template <int MODE, int NTOK, int BK>
+template <int MODE, int NTOK, int BK, bool PAIR = false>
 static int launch_t(const CUtensorMap& map, const CUtensorMap& ymap, const GemmParams& p, int grid,
                     cudaStream_t stream) {
-  using C = Cfg<MODE, NTOK, BK>;
-  auto kern = w4a8_gemm_kernel<MODE, NTOK, BK>;
+  using C = Cfg<MODE, NTOK, BK, PAIR>;
+  auto kern = w4a8_gemm_kernel<MODE, NTOK, BK, PAIR>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
@@ -1081,12 +1216,16 @@ static int launch_t(const CUtensorMap& map, const CUtensorMap& ymap, const GemmP
   lc.blockDim = dim3(C::kNumThreads);
   lc.dynamicSmemBytes = C::kSmemBytes;
   lc.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   static const int pdl = getenv("QQQ_NO_PDL") ? 0 : 1;  // developer A/B switch
   attr[0].val.programmaticStreamSerializationAllowed = pdl;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   lc.attrs = attr;
-  lc.numAttrs = 1;
+  lc.numAttrs = PAIR ? 2 : 1;
   return cudaLaunchKernelEx(&lc, kern, map, ymap, p) == cudaSuccess ? kOk : kErrCuda;
 }
 
@@ -1101,6 +1240,15 @@ static int launch_mode(int ntok, const CUtensorMap& map, const CUtensorMap& ymap
     case 256: return launch_t<MODE, 256, bk_for(MODE, 256)>(map, ymap, p, grid, st);
     default: return kErrConfig;
   }
+}
+
+template <int MODE>
+static int launch_pair(const CUtensorMap& map, const CUtensorMap& ymap, const GemmParams& p, int grid,
+                       cudaStream_t st) {
+  if constexpr (MODE == kModeI8)
+    return kErrConfig;
+  else
+    return launch_t<MODE, 256, kPairBk, true>(map, ymap, p, grid, st);
 }
 
 }  // namespace qqq
@@ -1147,7 +1295,7 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
 #ifdef QQQ_EXP_HALF_X
   cuuint32_t box[3] = {128u, (cuuint32_t)(lp.ntok >= 128 ? lp.ntok / 2 : lp.ntok), (cuuint32_t)(lp.bk / 128)};
 #else
-  cuuint32_t box[3] = {128u, (cuuint32_t)lp.ntok, (cuuint32_t)(lp.bk / 128)};
+  cuuint32_t box[3] = {128u, (cuuint32_t)(lp.pair ? lp.ntok / 2 : lp.ntok), (cuuint32_t)(lp.bk / 128)};
 #endif
   cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)aq, dims, strides, box, estr,
@@ -1196,8 +1344,16 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   p.aligned_tiles = lp.aligned_tiles;
   p.dp_tiles = lp.dp_tiles;
   p.sk_unit0 = lp.sk_unit0;
+  p.pair = lp.pair;
   p.dbg = cfg ? (unsigned long long*)cfg->dbg : nullptr;
 
+  if (lp.pair) {
+    switch (mode) {
+      case kModePC: return launch_pair<kModePC>(map, ymap, p, lp.grid, stream);
+      case kModePG: return launch_pair<kModePG>(map, ymap, p, lp.grid, stream);
+      default: return kErrConfig;
+    }
+  }
   switch (mode) {
     case kModePC: return launch_mode<kModePC>(lp.ntok, map, ymap, p, lp.grid, stream);
     case kModePG: return launch_mode<kModePG>(lp.ntok, map, ymap, p, lp.grid, stream);

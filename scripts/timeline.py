@@ -76,16 +76,18 @@ if a.pair:
             if v.size:
                 print(f"   {nm}: min/med/max {((v - t0) / 1e3).min():.2f}/{np.median((v - t0) / 1e3):.2f}/{((v - t0) / 1e3).max():.2f}")
     sys.exit(0)
-d = dbg.cpu().numpy().astype(np.int64)
-ctas = d[:, 0] > 0
-d = d[ctas]
-t0 = d[:, 0].min()
-print(f"{a.shape} M={a.m} {a.scheme} cfg={a.cfg} ctas={int(ctas.sum())}  (us relative to first CTA start)")
-order = sorted(NAMES, key=lambda sl: (sl >= 4 and sl < 20 or sl >= 64, sl))
-for slot in sorted(NAMES, key=lambda sl: ({20: 1}.get(sl // 16 * 16, 0), sl)):
-    col = d[:, slot]
-    v = col[col > 0]
-    if v.size == 0:
-        continue
-    r = (v - t0) / 1e3
-    print(f"  {NAMES[slot]:>10s}: n={v.size:4d} min={r.min():8.2f} med={np.median(r):8.2f} max={r.max():8.2f}")
+dall = dbg.cpu().numpy().astype(np.int64)
+t0 = dall[dall[:, 0] > 0, 0].min()
+# pair plans (split=3): even and odd CTAs of each cluster reported separately
+views = [("", dall)] if json.loads(a.cfg).get("split") != 3 else [("even CTAs ", dall[0::2]), ("odd CTAs ", dall[1::2])]
+for tag, d in views:
+    ctas = d[:, 0] > 0
+    d = d[ctas]
+    print(f"{tag}{a.shape} M={a.m} {a.scheme} cfg={a.cfg} ctas={int(ctas.sum())}  (us relative to first CTA start)")
+    for slot in sorted(NAMES, key=lambda sl: ({20: 1}.get(sl // 16 * 16, 0), sl)):
+        col = d[:, slot]
+        v = col[col > 0]
+        if v.size == 0:
+            continue
+        r = (v - t0) / 1e3
+        print(f"  {NAMES[slot]:>10s}: n={v.size:4d} min={r.min():8.2f} med={np.median(r):8.2f} max={r.max():8.2f}")

@@ -280,6 +280,24 @@ def test_gemm_all_tile_plans(ntok, split):
                 break
 
 
+@pytest.mark.parametrize("scheme,gs", [("per-channel", 0), ("per-group", 128), ("per-group", 32)])
+def test_gemm_pair_tiles(scheme, gs):
+    """2-CTA pair plan (split=3: tcgen05.mma.cta_group::2, 256-channel x 256-token
+    tiles): odd channel-tile counts, ragged tokens, partial last k-block, few pairs."""
+    for (m, k, n, grid) in ((77, 2304, 640, 0), (256, 1024, 384, 0), (300, 896, 1024, 0), (600, 1152, 1000, 7),
+                            (1, 256, 128, 0), (513, 4096, 256, 4)):
+        x16, qw_o = _rand_problem(m, k, n, scheme, gs or 128, seed=m + n)
+        aq_o = O.quant_act_per_token(x16.astype(np.float64))
+        run_o = O.w4a8_gemm_per_channel if scheme == "per-channel" else O.w4a8_gemm_per_group
+        want = run_o(aq_o, qw_o, O.FusedScales.from_quantized(qw_o), fast=True)
+        qw = _to_gpu_qw(qw_o)
+        prep = Q.gemm.prepare(qw, Q.FusedScales.from_quantized(qw))
+        aq = Q.quant_act_per_token(torch.from_numpy(x16).cuda())
+        out = Q.gemm.run_gemm(aq, prep, n, True, cfg={"ntok": 256, "split": 3, "grid": grid})
+        assert same_bits(out.acc, want.acc), (scheme, gs, m, k, n, grid)
+        assert same_bits(out.y, want.y), (scheme, gs, m, k, n, grid)
+
+
 def test_gemm_ragged_shapes():
     for (m, k, n, scheme, gs) in ((3, 33, 5, "per-channel", 0), (9, 100, 130, "per-channel", 0),
                                   (4, 96, 129, "per-group", 32), (2, 300, 1, "per-group", 100)):
