@@ -141,13 +141,20 @@ struct Cfg {
   // k-block ring depth: what is left after 3 weight stages, at most 4 and at
   // most the number of TMEM A buffers that fit beside the accumulators
   static constexpr int kXStagesRaw = (kRingBudget - 3 * kWBytes) / kXBytes;
-  static constexpr int kXCapWanted = PAIR ? 6 : 4;
+#ifndef QQQ_PAIR_XCAP
+#define QQQ_PAIR_XCAP 6
+#endif
+#ifndef QQQ_PAIR_WMAX
+#define QQQ_PAIR_WMAX 12
+#endif
+  static constexpr int kXCapWanted = PAIR ? QQQ_PAIR_XCAP : 4;
   static constexpr int kXCap = kABufsMax < kXCapWanted ? kABufsMax : kXCapWanted;
   static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > kXCap ? kXCap : kXStagesRaw);
   static constexpr int kABufs = kConvert ? kXStages : 0;
   static constexpr int kWStagesRaw = (kRingBudget - kXStages * kXBytes) / kWBytes;
   static_assert(kXStages <= kABufsMax || !kConvert, "TMEM A buffers");
-  static constexpr int kWStages = kWStagesRaw > 12 ? 12 : kWStagesRaw;
+  static constexpr int kWMax = PAIR ? QQQ_PAIR_WMAX : 12;
+  static constexpr int kWStages = kWStagesRaw > kWMax ? kWMax : kWStagesRaw;
   static_assert(kWStages >= 2, "shared memory budget too small");
   static constexpr int kOffX = 0;  // 1024-aligned: NTOK*BK is a multiple of 2048
   static constexpr int kOffW = kOffX + kXStages * kXBytes;
@@ -580,12 +587,13 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     if (lane == 0) QQQ_STAMP(3);
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
-    uint32_t s = 0, ph = 0;
+    uint32_t s = 0, ph = 0, xit = 0;
     while (si.next(tile, kb0, kb1)) {
       const int tok0 = (tile % p.tok_tiles) * NTOK;
 #pragma unroll 1
-      for (int kb = kb0; kb < kb1; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb, ++xit) {
         mbar_wait_sleep(&kb_empty[s], ph ^ 1);
+        if (lane == 0 && xit < 16) QQQ_STAMP(112 + xit);
         if (elect_one()) {
           if constexpr (PAIR) {
             // each CTA loads its half of the tokens; the bytes of both count on the even CTA's barrier
@@ -868,10 +876,14 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       }
       const bool owner = whole || seg_idx == 0;
       const int j = seg % C::kAccBufs;
-#ifdef QQQ_EPI_SLEEPWAIT
-      mbar_wait_sleep(&acc_full[j], (seg / C::kAccBufs) & 1);
-#else
+      // ONE warp polls the accumulator barrier (backoff), the others block in a
+      // named barrier: with every epilogue warp polling, the polls were ~40% of
+      // all instructions issued in a prefill kernel (ncu), taken from the converters
+#ifdef QQQ_EPI_ALLPOLL
       mbar_wait_backoff(&acc_full[j], (seg / C::kAccBufs) & 1);
+#else
+      if (warp == C::kEpiWarp0) mbar_wait_backoff(&acc_full[j], (seg / C::kAccBufs) & 1);
+      named_bar_sync(kBarAll, kAll);
 #endif
       tc_fence_after();
       if (lead && seg < 4) QQQ_STAMP(36 + 2 * seg);
@@ -1140,14 +1152,15 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
 }
 
 // Tile-plan cost model (us), fitted (log least squares, scripts/fit_planner.py)
-// to the B200 tile-plan sweep profiles/r01_tileplan_sweep_v2.jsonl of this
-// kernel (0.9% regret against the best measured plan over the C2 sweep):
+// to the B200 tile-plan sweeps profiles/r01_tileplan_sweep_v2.jsonl (decode /
+// mid M) and profiles/r01_pair_sweep.jsonl (prefill, incl. pair tiles) of this
+// kernel (1.2% regret against the best measured plan over both sweeps):
 //   per-k-block time u = max(weight bytes / per-CTA HBM share, conversion, MMA)
 //   whole tiles: T = T0 + units_per_CTA * u + waves * epilogue
 //   stream-K:    T = T0 + units_per_CTA * u + fix-up + epilogue
 static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
-  const double T0 = 1.714, kBsm = 218.7e3, kBtot = 11640e3, kConv = 14.36e-6, kMma = 1.461, kF0 = 1.87,
-               kF1 = 0.5761, kE0 = 3.524, kE1 = 0.004834;
+  const double T0 = 1.087, kBsm = 26.03e3, kBtot = 5379e3, kConv = 14.24e-6, kMma = 1.719, kF0 = 5.248,
+               kF1 = 0.3505, kE0 = 0.512, kE1 = 0.1027;
   const double clk = 1900.0;  // MHz
   const int cps = lp.ntok <= 64 ? 2 : 1;
   const int64_t ucta = lp.aligned_tiles > 0 ? (int64_t)lp.aligned_tiles * lp.kb_per_tile
@@ -1159,6 +1172,11 @@ static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
   const double u = std::max(std::max(wkb / bw, conv), mma);
   const double mt = (double)std::min<int64_t>(lp.ntok, M) / 16.0;
   const double epi = kE0 + kE1 * mt;
+  if (lp.pair) {
+    // 2-CTA pair tiles: ~0.41 us per 128-deep k-block of a 256x256 pair tile
+    const double kT0p = 1.41, kUp = 0.4133;
+    return kT0p + (double)lp.aligned_tiles * lp.kb_per_tile * kUp + lp.aligned_tiles * epi;
+  }
   if (lp.aligned_tiles > 0) return T0 + ucta * u + lp.aligned_tiles * epi;
   return T0 + ucta * u + kF0 + kF1 * mt + epi;
 }
@@ -1177,7 +1195,8 @@ static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force
   // measured faster at every M it would cover (r01_tileplan_sweep_v2)
   for (int nt : {16, 32, 128, 256}) {
     if (nt > 32 && nt / 4 >= M) break;  // a smaller tile already covers every token
-    for (int sk = 0; sk < 2; ++sk) {  // whole tiles / stream-K (the hybrid never won a sweep point)
+    for (int sk = 0; sk < 4; ++sk) {  // whole tiles / stream-K / pair tiles (the hybrid never won a sweep point)
+      if (sk == 2 || (sk == 3 && (nt != 256 || mode == kModeI8))) continue;
       const LaunchPlan lp = plan_for(mode, M, N, K, nt, sk, 0);
       if (lp.tiles > 65536) continue;
       const double t = plan_cost_us(lp, M);

@@ -7,6 +7,14 @@ from scipy.optimize import least_squares
 
 SMS = 148
 def plan(M, N, K, ntok, split):
+    if split == 3:  # 2-CTA pair tiles: 256 channels x 256 tokens, BK = 128, 74 pair slots
+        tok_tiles = -(-M // 256)
+        pairs = -(-(-(-N // 128)) // 2)
+        kbt = -(-K // 128)
+        tiles = pairs * tok_tiles
+        per = -(-tiles // (SMS // 2))
+        return dict(M=M, N=N, K=K, ntok=256, split=3, bk=128, cps=1, grid=2 * (-(-tiles // per)), ucta=per * kbt,
+                    kbt=kbt, tiles=tiles, waves=per)
     bk = 256
     cps = 2 if ntok <= 64 else 1
     slots = SMS * cps
@@ -28,8 +36,11 @@ def plan(M, N, K, ntok, split):
                 waves=waves)
 
 def cost(th, lp):
-    T0, Bsm, Btot, cconv, cmma, f0, f1, e0, e1 = th
+    T0, Bsm, Btot, cconv, cmma, f0, f1, e0, e1, T0p, Up = th
     clk = 1900.0
+    if lp['split'] == 3:
+        epi = e0 + e1 * min(256, lp['M']) / 16.0
+        return T0p + lp['ucta'] * Up + lp['waves'] * epi
     bw = min(Bsm * 1e3, Btot * 1e3 / lp['grid'])           # bytes/us per CTA
     wkb = lp['bk'] * 64.0 * (1 + 1 / 32)                   # packed weight bytes per k-block
     mma = (lp['bk'] / 32.0) * (lp['ntok'] / 2.0) / clk * cmma
@@ -42,11 +53,11 @@ def cost(th, lp):
     return T0 + lp['ucta'] * u + lp['waves'] * epi
 
 rows = []
-for l in open(sys.argv[1]):
+for l in (l for f in sys.argv[1:] for l in open(f)):
     if not l.startswith('{'):
         continue
     d = json.loads(l)
-    if d['cfg'] is None or d['cfg'].get('split', 1) == 2:
+    if d['cfg'] is None or d['cfg'].get('split', 1) == 2 or d['scheme'] != 'per-group':
         continue
     k, n = map(int, d['shape'].split('x'))
     rows.append((plan(d['M'], n, k, d['cfg']['ntok'], d['cfg']['split']), d['us']))
@@ -54,8 +65,9 @@ for l in open(sys.argv[1]):
 def resid(th):
     return np.array([math.log(cost(th, lp)) - math.log(t) for lp, t in rows])
 
-th0 = [2.5, 40.0, 6500.0, 25.0, 1.5, 2.0, 0.2, 1.0, 0.2]
-r = least_squares(resid, th0, bounds=([0, 1, 100, 0, 0.5, 0, 0, 0, 0], [20, 500, 20000, 500, 10, 50, 10, 20, 10]))
+th0 = [2.5, 40.0, 6500.0, 25.0, 1.5, 2.0, 0.2, 1.0, 0.2, 5.0, 0.35]
+r = least_squares(resid, th0, bounds=([0, 1, 100, 0, 0.5, 0, 0, 0, 0, 0, 0.05],
+                                      [20, 500, 20000, 500, 10, 50, 10, 20, 10, 30, 2]))
 th = r.x
 print("theta =", ", ".join("%.4g" % v for v in th))
 print("rms log err %.3f" % np.sqrt(np.mean(resid(th) ** 2)))
@@ -68,5 +80,5 @@ for key, g in sorted(groups.items()):
     pick = min(g, key=lambda x: x[0])
     tot_best += best[1]
     tot_pick += pick[1]
-    print(key, "best %d%s %.1f  pick %d%s %.1f" % (best[2], 'ws'[best[3]], best[1], pick[2], 'ws'[pick[3]], pick[1]))
+    print(key, "best %d%s %.1f  pick %d%s %.1f" % (best[2], 'ws?p'[best[3]], best[1], pick[2], 'ws?p'[pick[3]], pick[1]))
 print("sum best %.1f  sum picked %.1f  regret %.1f%%" % (tot_best, tot_pick, 100 * (tot_pick / tot_best - 1)))
