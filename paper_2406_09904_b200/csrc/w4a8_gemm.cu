@@ -62,6 +62,8 @@ struct GemmParams {
   int64_t sk_unit0;         //   its stream-K share of the units [sk_unit0, sk_unit0 + units)
   int y_tma;                // 1: y written by TMA stores from a shared-memory staging tile
   int pair;                 // 1: 2-CTA clusters (cta_group::2); tiles count 256-channel pair tiles
+  int csplit;               // >1: cluster split-K (decode CTAs): cluster c = tile c, rank r = k-range r of csplit,
+                            //     partials reduce-scattered over DSMEM (rank r finalizes channel rows r*128/csplit..)
   unsigned long long* dbg;  // optional per-CTA %globaltimer timeline, diagnostics only
 };
 
@@ -223,6 +225,15 @@ QQQ_DEVICE __half f64_to_f16_rn(double v) {
   return __ushort_as_half(h);
 }
 
+// 16 bytes into another cluster CTA's shared memory, completing 16 transaction
+// bytes on that CTA's mbarrier (both shared::cluster addresses)
+QQQ_DEVICE void st_async_v4(uint32_t cl_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t cl_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   cl_addr),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(cl_bar)
+               : "memory");
+}
+
 QQQ_DEVICE void red_add_s32(int32_t* p, int32_t v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -341,6 +352,12 @@ QQQ_DEVICE SegIter make_iter(const GemmParams& p) {
   SegIter it;
   it.kbt = p.kb_per_tile;
   it.v = it.v1 = 0;
+  if (p.csplit > 1) {  // cluster split-K: one tile per cluster, an even k-range per rank
+    const int c = blockIdx.x / p.csplit, r = blockIdx.x % p.csplit;
+    it.u = (int64_t)c * p.kb_per_tile + r * p.kb_per_tile / p.csplit;
+    it.u1 = (int64_t)c * p.kb_per_tile + (r + 1) * p.kb_per_tile / p.csplit;
+    return it;
+  }
   if (p.aligned_tiles > 0) {
     // pair plans: the CTA pair (2b, 2b+1) owns 256-channel pair tiles
     const int64_t tiles = (int64_t)(p.pair ? (p.n_tiles + 1) / 2 : p.n_tiles) * p.tok_tiles;
@@ -480,8 +497,8 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     }
   }
   tc_fence_before();
-  if constexpr (PAIR)
-    cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive / TMA signal
+  if (PAIR || (C::kSmall && p.csplit > 1))
+    cluster_sync_all();  // every cluster CTA's barriers initialised before any remote arrive / store
   else
     __syncthreads();
   tc_fence_after();
@@ -862,7 +879,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       named_bar_sync(kBarAll, kAll);
       const int n = n_tile * 128 + row;
       const bool n_ok = n < p.N;
-      const bool whole = (kb0 == 0 && kb1 == p.kb_per_tile);
+      const bool cs = C::kSmall && p.csplit > 1;  // cluster split-K: DSMEM reduce-scatter below
+#ifdef QQQ_EXP_NO_FIXUP
+      const bool whole = true;  // experiment: every segment stores its own partial (wrong results)
+#else
+      const bool whole = cs || (kb0 == 0 && kb1 == p.kb_per_tile);
+#endif
       const double s_col = (n_ok && p.s_col) ? p.s_col[n] : 0.0;
       int seg_idx = 0, nsegs = 1;
       int32_t* slots = nullptr;
@@ -876,6 +898,13 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       }
       const bool owner = whole || seg_idx == 0;
       const int j = seg % C::kAccBufs;
+      if (cs && lead) {
+        // this CTA finalizes channel rows [ceil(me*128/S), ceil((me+1)*128/S)): the
+        // other S-1 ranks each send those rows' NTOK int32 partials
+        const int S = p.csplit, me = (int)cluster_ctarank();
+        const int mine = ((me + 1) * 128 + S - 1) / S - (me * 128 + S - 1) / S;
+        mbar_arrive_expect_tx(&part_full[0], (uint32_t)((S - 1) * mine * NTOK * 4));
+      }
       // ONE warp polls the accumulator barrier (backoff), the others block in a
       // named barrier: with every epilogue warp polling, the polls were ~40% of
       // all instructions issued in a prefill kernel (ncu), taken from the converters
@@ -890,6 +919,75 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + j * NTOK;
       const int nchunks = (tvalid + 15) / 16;
       const int nmine = (nchunks - eh + H - 1) / H;  // chunks c = eh, eh + H, ...
+      if (cs) {
+        if constexpr (NTOK <= 32) {
+        // ---- cluster split-K: reduce-scatter the int32 partials over DSMEM. The
+        // thread of channel row `row` sends its NTOK partials to the rank that
+        // finalizes the row (st.async, completing bytes on that rank's barrier);
+        // the finalizing rank adds the S-1 received partials to its own, applies
+        // the dequant and stores y directly (a few rows per CTA).
+        const int S = p.csplit, me = (int)cluster_ctarank();
+        const int dest = row * S / 128;
+        const int rows_per = (128 + S - 1) / S;
+        const int drow0 = (dest * 128 + S - 1) / S;
+        int32_t* recv = reinterpret_cast<int32_t*>(pstage);  // [S][rows_per][NTOK]
+        uint32_t own[NTOK];
+#pragma unroll
+        for (int c0 = 0; c0 < NTOK; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(taddr + c0, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) own[c0 + i] = r[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[j]);
+        if (dest != me) {
+          const uint32_t dst = mapa_shared(recv + (me * rows_per + (row - drow0)) * NTOK, (uint32_t)dest);
+          const uint32_t dbar = mapa_shared(&part_full[0], (uint32_t)dest);
+#pragma unroll
+          for (int i = 0; i < NTOK; i += 4) st_async_v4(dst + i * 4, own[i], own[i + 1], own[i + 2], own[i + 3], dbar);
+        } else {
+          mbar_wait(&part_full[0], seg & 1);
+          const int lr = row - drow0;
+#pragma unroll 1
+          for (int sg = 0; sg < S; ++sg) {
+            if (sg == me) continue;
+            const int32_t* src = recv + (sg * rows_per + lr) * NTOK;
+#pragma unroll
+            for (int i = 0; i < NTOK; ++i) own[i] += (uint32_t)src[i];
+          }
+          if (n_ok) {
+#pragma unroll
+            for (int c0 = 0; c0 < NTOK; c0 += 16) {
+              if (c0 >= tvalid) break;
+              uint32_t r[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                r[i] = own[c0 + i];
+                if constexpr (C::kU8) r[i] -= (uint32_t)rs_smem[c0 + i];  // u8 weights carried +128
+              }
+              if (p.acc) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                  if (c0 + i < tvalid) p.acc[(int64_t)(tok0 + c0 + i) * p.ldacc + n] = (int32_t)r[i];
+              }
+              if (p.s_col) {
+                uint16_t h[16];
+                dequant16(r, sa_smem + c0, s_col, h, tvalid - c0);
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                  if (c0 + i < tvalid) reinterpret_cast<uint16_t*>(p.y)[(int64_t)(tok0 + c0 + i) * p.ldy + n] = h[i];
+              }
+            }
+          }
+        }
+        }  // NTOK <= 32
+        if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
+        ++seg;
+        continue;
+      }
       if (!owner) {
         // ---- contributor: add the partial into the tile's slot, release the counter.
         // Chunks with few valid tokens use per-element red.add; fuller chunks are
@@ -949,7 +1047,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           named_bar_sync(kBarAll, kAll);
         }
         // reduced partial chunks [16 tok][128 rows] int32 (8 KiB, contiguous in the
-        // slot) are bulk-copied into this half's 2-deep smem ring, one chunk ahead
+        // slot) are bulk-copied into this half's PB-deep smem ring, PB chunks ahead
         auto part_issue = [&](int li) {
           const uint32_t pc = pchunk + li;
           mbar_arrive_expect_tx(&pfull[pc % PB], 8192);
@@ -1021,9 +1119,9 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     if (lead) QQQ_STAMP(63);
   }
 
-  if constexpr (PAIR) {
-    // no CTA of the pair retires while the other may still signal its barriers
-    // or the pair MMAs may still read its shared memory / TMEM
+  if (PAIR || (C::kSmall && p.csplit > 1)) {
+    // no CTA of the cluster retires while another may still signal its barriers,
+    // store into its shared memory or (pair) read its shared memory / TMEM
     tc_fence_before();
     cluster_sync_all();
   } else {
@@ -1070,7 +1168,7 @@ static int num_sms() {
 }
 
 struct LaunchPlan {
-  int ntok, bk, grid, aligned_tiles, tok_tiles, n_tiles, kb_per_tile, tiles, max_segs, dp_tiles, pair;
+  int ntok, bk, grid, aligned_tiles, tok_tiles, n_tiles, kb_per_tile, tiles, max_segs, dp_tiles, pair, csplit;
   int64_t units, sk_unit0;
 };
 
@@ -1092,6 +1190,30 @@ static constexpr int kPairBk = QQQ_PAIR_BK;
 //        3 = whole 256-channel pair tiles on 2-CTA clusters (NTOK = 256, PC/PG)
 static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, int split, int force_grid) {
   LaunchPlan lp{};
+  if (split == 4 && (ntok > 32 || ctas_per_sm(mode, ntok) != 2)) split = 1;
+  if (split == 4) {
+    // cluster split-K: one tile per cluster of S decode CTAs, S in {8, 4, 2}: the
+    // largest that fits the CTA slots and leaves every rank >= 1 k-block
+    lp.ntok = ntok;
+    lp.bk = bk_for(mode, ntok);
+    lp.tok_tiles = (int)((M + ntok - 1) / ntok);
+    lp.n_tiles = (int)(round_up(N, kTileN) / kTileN);
+    lp.kb_per_tile = (int)((round_up(K, kKPadTo) + lp.bk - 1) / lp.bk);
+    lp.tiles = lp.n_tiles * lp.tok_tiles;
+    lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
+    lp.max_segs = 1;
+    const int slots = num_sms() * ctas_per_sm(mode, ntok);
+    int S = 1;
+    for (int c : {8, 4, 2})
+      if ((int64_t)lp.tiles * c <= slots && c <= lp.kb_per_tile) {
+        S = c;
+        break;
+      }
+    if (S == 1) return plan_for(mode, M, N, K, ntok, 1, force_grid);
+    lp.csplit = S;
+    lp.grid = lp.tiles * S;
+    return lp;
+  }
   if (split == 3 && (ntok != 256 || mode == kModeI8)) split = 0;
   if (split == 3) {
     lp.ntok = ntok;
@@ -1172,6 +1294,14 @@ static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
   const double u = std::max(std::max(wkb / bw, conv), mma);
   const double mt = (double)std::min<int64_t>(lp.ntok, M) / 16.0;
   const double epi = kE0 + kE1 * mt;
+  if (lp.csplit > 1) {
+    // cluster split-K (linear fit to profiles/r01_decode_sweep.jsonl, 7% rms): a
+    // fixed cost, the per-CTA k-blocks scaled by the CTA-slot occupancy (the
+    // decode stream shares HBM), +2.4 us for the 32-token tile (2 weight stages)
+    const int ucta_cs = (lp.kb_per_tile + lp.csplit - 1) / lp.csplit;
+    const double occ = (double)lp.grid / (num_sms() * 2);
+    return 5.138 + 1.079 * occ * ucta_cs + (lp.ntok == 32 ? 2.412 : 0.0) + 0.051 * mt;
+  }
   if (lp.pair) {
     // 2-CTA pair tiles: ~0.41 us per 128-deep k-block of a 256x256 pair tile
     const double kT0p = 1.41, kUp = 0.4133;
@@ -1195,8 +1325,10 @@ static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force
   // measured faster at every M it would cover (r01_tileplan_sweep_v2)
   for (int nt : {16, 32, 128, 256}) {
     if (nt > 32 && nt / 4 >= M) break;  // a smaller tile already covers every token
-    for (int sk = 0; sk < 4; ++sk) {  // whole tiles / stream-K / pair tiles (the hybrid never won a sweep point)
-      if (sk == 2 || (sk == 3 && (nt != 256 || mode == kModeI8))) continue;
+    // whole tiles / stream-K / pair tiles / cluster split-K (the hybrid never won a sweep point)
+    for (int sk = 0; sk < 5; ++sk) {
+      if (sk == 2 || (sk == 3 && (nt != 256 || mode == kModeI8)) || (sk == 4 && (nt > 32 || mode == kModeI8)))
+        continue;
       const LaunchPlan lp = plan_for(mode, M, N, K, nt, sk, 0);
       if (lp.tiles > 65536) continue;
       const double t = plan_cost_us(lp, M);
@@ -1215,7 +1347,7 @@ constexpr int kMaxTiles = 65536;
 constexpr size_t kCounterBytes = (size_t)kMaxTiles * 4;
 
 static size_t plan_ws_bytes(const LaunchPlan& lp) {
-  if (lp.aligned_tiles > 0) return kCounterBytes;
+  if (lp.aligned_tiles > 0 || lp.csplit > 1) return kCounterBytes;
   return kCounterBytes + (size_t)lp.tiles * lp.ntok * 128 * 4;
 }
 
@@ -1240,11 +1372,11 @@ static int launch_t(const CUtensorMap& map, const CUtensorMap& ymap, const GemmP
   static const int pdl = getenv("QQQ_NO_PDL") ? 0 : 1;  // developer A/B switch
   attr[0].val.programmaticStreamSerializationAllowed = pdl;
   attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[1].val.clusterDim.x = PAIR ? 2 : (p.csplit > 1 ? p.csplit : 1);
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = 1;
   lc.attrs = attr;
-  lc.numAttrs = PAIR ? 2 : 1;
+  lc.numAttrs = (PAIR || p.csplit > 1) ? 2 : 1;
   return cudaLaunchKernelEx(&lc, kern, map, ymap, p) == cudaSuccess ? kOk : kErrCuda;
 }
 
@@ -1364,6 +1496,7 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   p.dp_tiles = lp.dp_tiles;
   p.sk_unit0 = lp.sk_unit0;
   p.pair = lp.pair;
+  p.csplit = lp.csplit;
   p.dbg = cfg ? (unsigned long long*)cfg->dbg : nullptr;
 
   if (lp.pair) {

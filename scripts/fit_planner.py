@@ -17,6 +17,16 @@ def plan(M, N, K, ntok, split):
                     kbt=kbt, tiles=tiles, waves=per)
     bk = 256
     cps = 2 if ntok <= 64 else 1
+    if split == 4:  # cluster split-K: one tile per cluster of S decode CTAs
+        tok_tiles = -(-M // ntok)
+        n_tiles = -(-N // 128)
+        kbt = -(-K // 256)
+        tiles = n_tiles * tok_tiles
+        S = next((c for c in (8, 4, 2) if tiles * c <= SMS * 2 and c <= kbt), 1)
+        if S == 1:
+            return plan(M, N, K, ntok, 1)
+        return dict(M=M, N=N, K=K, ntok=ntok, split=4, bk=bk, cps=2, grid=tiles * S, ucta=-(-kbt // S), kbt=kbt,
+                    tiles=tiles, waves=1, S=S)
     slots = SMS * cps
     tok_tiles = -(-M // ntok)
     n_tiles = -(-N // 128)
@@ -36,7 +46,7 @@ def plan(M, N, K, ntok, split):
                 waves=waves)
 
 def cost(th, lp):
-    T0, Bsm, Btot, cconv, cmma, f0, f1, e0, e1, T0p, Up = th
+    T0, Bsm, Btot, cconv, cmma, f0, f1, e0, e1, T0p, Up, c0, c1 = th
     clk = 1900.0
     if lp['split'] == 3:
         epi = e0 + e1 * min(256, lp['M']) / 16.0
@@ -47,6 +57,8 @@ def cost(th, lp):
     conv = lp['bk'] * 128.0 * cconv * 1e-6 * lp['cps']
     u = max(wkb / bw, conv, mma)
     epi = e0 + e1 * min(lp['ntok'], lp['M']) / 16.0
+    if lp['split'] == 4:  # no cross-CTA fix-up; cluster launch / DSMEM exchange
+        return T0 + c0 + lp['ucta'] * u + epi + c1 * min(lp['ntok'], lp['M']) / 16.0
     if lp['split'] == 1:
         fix = f0 + f1 * min(lp['ntok'], lp['M']) / 16.0
         return T0 + lp['ucta'] * u + fix + epi
@@ -65,9 +77,9 @@ for l in (l for f in sys.argv[1:] for l in open(f)):
 def resid(th):
     return np.array([math.log(cost(th, lp)) - math.log(t) for lp, t in rows])
 
-th0 = [2.5, 40.0, 6500.0, 25.0, 1.5, 2.0, 0.2, 1.0, 0.2, 5.0, 0.35]
-r = least_squares(resid, th0, bounds=([0, 1, 100, 0, 0.5, 0, 0, 0, 0, 0, 0.05],
-                                      [20, 500, 20000, 500, 10, 50, 10, 20, 10, 30, 2]))
+th0 = [2.5, 40.0, 6500.0, 25.0, 1.5, 2.0, 0.2, 1.0, 0.2, 5.0, 0.35, 0.5, 0.1]
+r = least_squares(resid, th0, bounds=([0, 1, 100, 0, 0.5, 0, 0, 0, 0, 0, 0.05, -5, -5],
+                                      [20, 500, 20000, 500, 10, 50, 10, 20, 10, 30, 2, 10, 10]))
 th = r.x
 print("theta =", ", ".join("%.4g" % v for v in th))
 print("rms log err %.3f" % np.sqrt(np.mean(resid(th) ** 2)))
@@ -80,5 +92,5 @@ for key, g in sorted(groups.items()):
     pick = min(g, key=lambda x: x[0])
     tot_best += best[1]
     tot_pick += pick[1]
-    print(key, "best %d%s %.1f  pick %d%s %.1f" % (best[2], 'ws?p'[best[3]], best[1], pick[2], 'ws?p'[pick[3]], pick[1]))
+    print(key, "best %d%s %.1f  pick %d%s %.1f" % (best[2], 'ws?pc'[best[3]], best[1], pick[2], 'ws?pc'[pick[3]], pick[1]))
 print("sum best %.1f  sum picked %.1f  regret %.1f%%" % (tot_best, tot_pick, 100 * (tot_pick / tot_best - 1)))

@@ -298,6 +298,25 @@ def test_gemm_pair_tiles(scheme, gs):
         assert same_bits(out.y, want.y), (scheme, gs, m, k, n, grid)
 
 
+@pytest.mark.parametrize("scheme,gs", [("per-channel", 0), ("per-group", 128), ("per-group", 32)])
+@pytest.mark.parametrize("ntok", [16, 32])
+def test_gemm_cluster_splitk(scheme, gs, ntok):
+    """Cluster split-K plan (split=4): one tile per cluster of S in {8, 4, 2} decode
+    CTAs, int32 partials reduce-scattered over DSMEM; ragged M, partial last k-block."""
+    for (m, k, n) in ((1, 4096, 4096), (16, 2048, 11008), (5, 1024, 640), (31, 2304, 384), (13, 4352, 256)):
+        x16, qw_o = _rand_problem(m, k, n, scheme, gs or 128, seed=m * 7 + n)
+        aq_o = O.quant_act_per_token(x16.astype(np.float64))
+        run_o = O.w4a8_gemm_per_channel if scheme == "per-channel" else O.w4a8_gemm_per_group
+        want = run_o(aq_o, qw_o, O.FusedScales.from_quantized(qw_o), fast=True)
+        qw = _to_gpu_qw(qw_o)
+        prep = Q.gemm.prepare(qw, Q.FusedScales.from_quantized(qw))
+        aq = Q.quant_act_per_token(torch.from_numpy(x16).cuda())
+        for _ in range(2):  # second launch: the plan leaves no state behind
+            out = Q.gemm.run_gemm(aq, prep, n, True, cfg={"ntok": ntok, "split": 4})
+            assert same_bits(out.acc, want.acc), (scheme, gs, ntok, m, k, n)
+            assert same_bits(out.y, want.y), (scheme, gs, ntok, m, k, n)
+
+
 def test_gemm_ragged_shapes():
     for (m, k, n, scheme, gs) in ((3, 33, 5, "per-channel", 0), (9, 100, 130, "per-channel", 0),
                                   (4, 96, 129, "per-group", 32), (2, 300, 1, "per-group", 100)):
