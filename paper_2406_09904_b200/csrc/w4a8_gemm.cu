@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     }
   }
   tc_fence_before();
-  if (PAIR || (C::kSmall && p.csplit > 1))
+  if (PAIR || p.csplit > 1)
     cluster_sync_all();  // every cluster CTA's barriers initialised before any remote arrive / store
   else
     __syncthreads();
@@ -1119,7 +1119,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     if (lead) QQQ_STAMP(63);
   }
 
-  if (PAIR || (C::kSmall && p.csplit > 1)) {
+  if (PAIR || p.csplit > 1) {
     // no CTA of the cluster retires while another may still signal its barriers,
     // store into its shared memory or (pair) read its shared memory / TMEM
     tc_fence_before();
@@ -1190,6 +1190,9 @@ static constexpr int kPairBk = QQQ_PAIR_BK;
 //        3 = whole 256-channel pair tiles on 2-CTA clusters (NTOK = 256, PC/PG)
 static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, int split, int force_grid) {
   LaunchPlan lp{};
+  // cluster split-K: decode tiles only (NTOK 16/32, 2 CTAs per SM). (A 128-token
+  // prefill variant — 64 KiB partials over DSMEM — measured slower than stream-K:
+  // the exchange ran at ~7 B/clk per SM.)
   if (split == 4 && (ntok > 32 || ctas_per_sm(mode, ntok) != 2)) split = 1;
   if (split == 4) {
     // cluster split-K: one tile per cluster of S decode CTAs, S in {8, 4, 2}: the
@@ -1202,7 +1205,7 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
     lp.tiles = lp.n_tiles * lp.tok_tiles;
     lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
     lp.max_segs = 1;
-    const int slots = num_sms() * ctas_per_sm(mode, ntok);
+    const int slots = (force_grid > 0 ? std::min(force_grid, num_sms()) : num_sms()) * ctas_per_sm(mode, ntok);
     int S = 1;
     for (int c : {8, 4, 2})
       if ((int64_t)lp.tiles * c <= slots && c <= lp.kb_per_tile) {
