@@ -242,24 +242,48 @@ __global__ void __launch_bounds__(kThreads) act_quant_row_kernel(const __half* _
   for (int j = 0; j < kVPT; ++j) {
     const int64_t i = threadIdx.x + (int64_t)j * kThreads;
     mb[j] = (kSmooth && smooth_mask != nullptr && i < nv) ? (uint32_t)__ldg(smooth_mask + i) : 0u;
+    // the smoothing values are consumed vector by vector below: start all their
+    // fetches now (no registers held) so those loads hit L1
+    if (kSmooth && smooth_mask == nullptr && i < nv) asm volatile("prefetch.global.L1 [%0];" ::"l"(smooth + i * 8));
   }
   Acc m = Acc(0);
   bool bad = false;
+  // smoothed rows: the quotients x / s_k (IEEE f64 division, once per element,
+  // unconditionally — x / 1.0 == x, and a per-lane `s_k == 1` branch diverges in
+  // nearly every warp anyway) stay in registers for the code pass; s_k is read
+  // as 16-byte pairs
+  double xs[kSmooth ? kVPT : 1][8];
 #pragma unroll
   for (int j = 0; j < kVPT; ++j) {
     const int64_t i = threadIdx.x + (int64_t)j * kThreads;
     if (i < nv) {
       const __half* e = reinterpret_cast<const __half*>(&v[j]);
+      if constexpr (kSmooth) {
+        double sk[8];
+        if (smooth_mask == nullptr) {
+          const double2* sv = reinterpret_cast<const double2*>(smooth + i * 8);  // 64 B per vector
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        Acc a;
-        if constexpr (kSmooth) {
-          a = fabs(sdiv((double)__half2float(e[t]), i, t, mb[j]));
-        } else {
-          a = absval(e[t]);
+          for (int h = 0; h < 4; ++h) {
+            const double2 d = __ldg(sv + h);
+            sk[2 * h] = d.x;
+            sk[2 * h + 1] = d.y;
+          }
         }
-        bad |= is_bad(a);
-        m = a > m ? a : m;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const double xv = (double)__half2float(e[t]);
+          xs[j][t] = smooth_mask == nullptr ? xv / sk[t] : sdiv(xv, i, t, mb[j]);
+          const Acc a = fabs(xs[j][t]);
+          bad |= is_bad(a);
+          m = a > m ? a : m;
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const Acc a = absval(e[t]);
+          bad |= is_bad(a);
+          m = a > m ? a : m;
+        }
       }
     }
   }
@@ -285,7 +309,7 @@ __global__ void __launch_bounds__(kThreads) act_quant_row_kernel(const __half* _
         int8_t c = 0;
         if (!zero_row) {
           if constexpr (kSmooth) {
-            c = quant_code_f64(sdiv((double)__half2float(e[t]), i, t, mb[j]), inv64, s);
+            c = quant_code_f64(xs[j][t], inv64, s);
           } else {
             c = quant_code_f16(__half2float(e[t]), inv, s);
           }
@@ -304,6 +328,142 @@ __global__ void __launch_bounds__(kThreads) act_quant_row_kernel(const __half* _
       int t = 0;
       for (int w = 0; w < kThreads / 32; ++w) t += isum[w];
       rowsum_out[row] = t;
+    }
+  }
+}
+
+QQQ_DEVICE uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+QQQ_DEVICE void st_async_b64(uint32_t cl_addr, uint64_t v, uint32_t cl_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(cl_addr), "l"(v),
+               "r"(cl_bar)
+               : "memory");
+}
+QQQ_DEVICE void st_async_b32(uint32_t cl_addr, uint32_t v, uint32_t cl_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(cl_addr), "r"(v),
+               "r"(cl_bar)
+               : "memory");
+}
+
+// Small-M variant (decode batches): a token row is split over a cluster of G =
+// ceil(K/8 / kThreads) CTAs, one 16-byte vector per thread, so the per-thread
+// dependent work is one vector instead of up to 4 (the row kernel's latency is
+// instruction-bound: ~135 instructions per element with the smoothing
+// division). The CTAs exchange their partial absmax (st.async into every
+// peer's shared memory, completing on its mbarrier) and their code sums (into
+// rank 0, which writes s_a and rowsum). Same arithmetic as the row kernel.
+template <int kThreads, bool kSmooth>
+__global__ void __launch_bounds__(kThreads) act_quant_cluster_kernel(const __half* __restrict__ x, int64_t K,
+                                                                      int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
+                                                                      double* __restrict__ s_out, int32_t* status,
+                                                                      int32_t* __restrict__ rowsum_out,
+                                                                      const double* __restrict__ smooth) {
+  using Acc = typename std::conditional<kSmooth, double, float>::type;
+  __shared__ uint64_t bar[2];       // [0] peer maxima landed, [1] (rank 0) peer code sums landed
+  __shared__ double peer_max[8];
+  __shared__ int32_t peer_sum[8];
+  __shared__ Acc red[32];
+  __shared__ int isum[kThreads / 32];
+  const uint32_t G = cluster_nctarank(), rank = cluster_ctarank();
+  const int64_t row = blockIdx.x / G;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  cluster_sync_all();  // every CTA's barriers initialised before any st.async targets them
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t nv = K / 8;
+  const int64_t v0 = rank * nv / G, v1 = (rank + 1) * nv / G;
+  const int64_t i = v0 + threadIdx.x;
+  const bool has = i < v1;
+  uint4 v = has ? __ldg(reinterpret_cast<const uint4*>(x + row * ldx) + i) : make_uint4(0, 0, 0, 0);
+  double sk[8];
+  if constexpr (kSmooth) {
+    if (has) {
+      const double2* sv = reinterpret_cast<const double2*>(smooth + i * 8);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 d = __ldg(sv + h);
+        sk[2 * h] = d.x;
+        sk[2 * h + 1] = d.y;
+      }
+    }
+  }
+  const __half* e = reinterpret_cast<const __half*>(&v);
+  Acc xs[8];
+  Acc m = Acc(0);
+  bool bad = false;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    if constexpr (kSmooth) {
+      xs[t] = has ? (double)__half2float(e[t]) / sk[t] : 0.0;
+    } else {
+      xs[t] = __half2float(e[t]);
+    }
+    const Acc a = fabs(xs[t]);
+    bad |= is_bad(a);
+    m = a > m ? a : m;
+  }
+  if (__syncthreads_or(bad)) {
+    if (threadIdx.x == 0) atomicOr(status, kStatNonFinite);
+  }
+  m = block_max<kThreads, Acc>(m, red);
+  if (threadIdx.x == 0) {
+    const double md = (double)m;
+    peer_max[rank] = md;
+    if (G > 1) {
+      mbar_arrive_expect_tx(&bar[0], (G - 1) * 8);
+      for (uint32_t d = 0; d < G; ++d)
+        if (d != rank)
+          st_async_b64(mapa_shared(&peer_max[rank], d), __double_as_longlong(md), mapa_shared(&bar[0], d));
+      mbar_wait(&bar[0], 0);
+    }
+  }
+  __syncthreads();
+  Acc mr = Acc(0);
+  for (uint32_t d = 0; d < G; ++d) mr = (Acc)peer_max[d] > mr ? (Acc)peer_max[d] : mr;
+  const double s = (mr > Acc(0)) ? (double)mr / 127.0 : 1.0;
+  const bool zero_row = !(mr > Acc(0));
+  const float inv = zero_row ? 0.0f : 127.0f / (float)mr;
+  const double inv64 = 1.0 / s;
+  int csum = 0;
+  if (has) {
+    alignas(8) int8_t out[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      int8_t c = 0;
+      if (!zero_row) {
+        if constexpr (kSmooth)
+          c = quant_code_f64(xs[t], inv64, s);
+        else
+          c = quant_code_f16(xs[t], inv, s);
+      }
+      out[t] = c;
+      csum += c;
+    }
+    *reinterpret_cast<uint2*>(q + row * ldq + i * 8) = *reinterpret_cast<const uint2*>(out);
+  }
+  for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+  if ((threadIdx.x & 31) == 0) isum[threadIdx.x >> 5] = csum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < kThreads / 32; ++w) t += isum[w];
+    if (rank != 0) {
+      st_async_b32(mapa_shared(&peer_sum[rank], 0), (uint32_t)t, mapa_shared(&bar[1], 0));
+    } else {
+      if (G > 1) {
+        mbar_arrive_expect_tx(&bar[1], (G - 1) * 4);
+        mbar_wait(&bar[1], 0);
+        for (uint32_t d = 1; d < G; ++d) t += peer_sum[d];
+      }
+      s_out[row] = s;
+      if (rowsum_out) rowsum_out[row] = t;
     }
   }
 }
@@ -345,11 +505,35 @@ static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, in
   lc.attrs = attr;
   lc.numAttrs = 1;
   cudaError_t e;
+  // small M (decode batches), smoothed fp16 rows up to 8 x 256 vectors: row split over
+  // a cluster (measured: 4.7 vs 5.2 us per smoothed M=1 quantizer in the C4 chain; the
+  // plain quantizer's ~35 instructions per element gain nothing from it)
+  constexpr int kCT = 256;
+  if (smooth && x_dtype == 0 && !row_max_in && !row_max_out && !smooth_mask && M <= 64 && K % 8 == 0 &&
+      K <= (int64_t)8 * kCT * 8 && ldx % 8 == 0 && ldq % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(q) & 7) == 0 && (reinterpret_cast<uintptr_t>(smooth) & 15) == 0) {
+    const int G = (int)((K / 8 + kCT - 1) / kCT);
+    cudaLaunchAttribute ca[2];
+    ca[0] = attr[0];
+    ca[1].id = cudaLaunchAttributeClusterDimension;
+    ca[1].val.clusterDim.x = G;
+    ca[1].val.clusterDim.y = 1;
+    ca[1].val.clusterDim.z = 1;
+    cudaLaunchConfig_t cc = lc;
+    cc.gridDim = dim3((unsigned)(M * G));
+    cc.blockDim = dim3(kCT);
+    cc.attrs = ca;
+    cc.numAttrs = 2;
+    e = cudaLaunchKernelEx(&cc, act_quant_cluster_kernel<kCT, true>, (const __half*)x, K, ldx, q, ldq, s_a,
+                           status_dev, rowsum, smooth);
+    return e == cudaSuccess ? kOk : kErrCuda;
+  }
   // fp16 rows that fit one CTA's registers: the single-round-trip kernel
   constexpr int kRT = 512, kRV = 4;
   if (x_dtype == 0 && !row_max_in && !row_max_out && K % 8 == 0 &&
       K <= (int64_t)kRT * kRV * 8 && ldx % 8 == 0 &&
-      ldq % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(q) & 7) == 0) {
+      ldq % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(q) & 7) == 0 &&
+      (reinterpret_cast<uintptr_t>(smooth) & 15) == 0) {  // (smoothing vector read as 16-byte pairs)
     lc.blockDim = dim3(kRT);
     if (smooth)
       e = cudaLaunchKernelEx(&lc, act_quant_row_kernel<kRT, kRV, true>, (const __half*)x, K, ldx, q, ldq, s_a,

@@ -76,3 +76,25 @@ def test_gpu_apply_quant_linear_errors():
     x[1, 3] = float("inf")
     with pytest.raises(Q.DataError):
         Q.quant_act_smoothed(x, np.ones(128))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [4096, 11008, 13000])
+def test_gpu_quant_act_smoothed_random_vs_oracle(k):
+    """The register-resident smoothed quantizer (one IEEE f64 division per
+    element) against the oracle's quant_act_per_token(x / s) on random rows,
+    ~1/8 of the channels smoothed (pipeline.py:146)."""
+    import torch
+
+    import paper_2406_09904_b200 as Q
+
+    rng = np.random.default_rng(k)
+    for m in (1, 3, 64):
+        x16 = (rng.standard_normal((m, k)) * rng.uniform(0.1, 8.0, (m, 1))).astype(np.float16)
+        s = np.ones(k)
+        sel = rng.choice(k, k // 8, replace=False)
+        s[sel] = rng.uniform(0.05, 20.0, k // 8)
+        want = O.quant_act_per_token(x16.astype(np.float64) / s)
+        got = Q.quant_act_smoothed(torch.from_numpy(x16).cuda(), s)
+        assert np.array_equal(got.q.cpu().numpy(), want.q), (k, m)
+        assert np.array_equal(got.s_a.cpu().numpy().view(np.uint64), want.s_a.view(np.uint64)), (k, m)
