@@ -120,7 +120,7 @@ struct Cfg {
   static constexpr int kTmemBudget = kSmall ? 256 : 512;
   // split-K partial ring depth per epilogue group (2 when the shared memory allows)
   // (the NTOK=256 prefill tiles, mostly whole tiles, give it up for activation stages)
-  static constexpr int kPartBufs = (kEpiGroups > 2 && NTOK >= 256) ? 1 : 2;
+  static constexpr int kPartBufs = (kEpiGroups > 2 && NTOK >= 256) ? 1 : 2;  // (part_full holds 2 per group)
   static constexpr int kEpiSmem = kNumEpiWarps * 2048 + kEpiGroups * kPartBufs * 8192;  // y staging + partial ring
   // Two rings. Weights: their own TMA ring (released by the converters once
   // the packed bytes are consumed, or by the MMA in I8 mode). K-blocks: ring
@@ -368,12 +368,14 @@ QQQ_DEVICE SegIter make_iter(const GemmParams& p) {
     it.u = t0 * p.kb_per_tile;
     it.u1 = t1 * p.kb_per_tile;
   } else {
-    it.u = p.sk_unit0 + (int64_t)blockIdx.x * p.units / gridDim.x;
-    it.u1 = p.sk_unit0 + (int64_t)(blockIdx.x + 1) * p.units / gridDim.x;
+    // (pair plans: the stream-K "CTA" is the CTA pair; both CTAs take the same units)
+    const int64_t b = p.pair ? blockIdx.x >> 1 : blockIdx.x, G = p.pair ? gridDim.x >> 1 : gridDim.x;
+    it.u = p.sk_unit0 + b * p.units / G;
+    it.u1 = p.sk_unit0 + (b + 1) * p.units / G;
     if (p.dp_tiles > 0) {
       it.v = it.u;
       it.v1 = it.u1;
-      it.u = (int64_t)blockIdx.x * p.dp_tiles * p.kb_per_tile;
+      it.u = b * p.dp_tiles * p.kb_per_tile;
       it.u1 = it.u + (int64_t)p.dp_tiles * p.kb_per_tile;
     }
   }
@@ -888,13 +890,17 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       const double s_col = (n_ok && p.s_col) ? p.s_col[n] : 0.0;
       int seg_idx = 0, nsegs = 1;
       int32_t* slots = nullptr;
+      // pair plans: segments are counted in CTA pairs; each CTA of a pair reduces its
+      // own 128 channels in its own slot / counter (index tile * 2 + rank)
+      const int slot_id = PAIR ? tile * 2 + (int)crank : tile;
       if (!whole) {
         const int64_t u_first = (int64_t)tile * p.kb_per_tile;
-        const int b_first = cta_of_unit(u_first, p, gridDim.x);
-        const int b_last = cta_of_unit(u_first + p.kb_per_tile - 1, p, gridDim.x);
-        seg_idx = (int)blockIdx.x - b_first;
+        const int G = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+        const int b_first = cta_of_unit(u_first, p, G);
+        const int b_last = cta_of_unit(u_first + p.kb_per_tile - 1, p, G);
+        seg_idx = (PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x) - b_first;
         nsegs = b_last - b_first + 1;
-        slots = p.ws + (int64_t)tile * NTOK * 128;  // one zero-initialised accumulation slot per tile
+        slots = p.ws + (int64_t)slot_id * NTOK * 128;  // one zero-initialised accumulation slot per tile
       }
       const bool owner = whole || seg_idx == 0;
       const int j = seg % C::kAccBufs;
@@ -1021,7 +1027,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[j]);
+        if (lane == 0) {
+          if constexpr (PAIR)
+            mbar_arrive_cluster(acc_empty_cl + j * 8);
+          else
+            mbar_arrive(&acc_empty[j]);
+        }
         // publish: the group leads wait for their bulk reductions to complete, then
         // CTA barrier and ONE gpu-scope release by the lead (cumulative over the
         // red.adds / completed bulk reductions ordered before it by the barrier)
@@ -1030,13 +1041,13 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         named_bar_sync(kBarAll, kAll);
-        if (lead) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + tile) : "memory");
+        if (lead) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.counters + slot_id) : "memory");
         if (lead) QQQ_STAMP(61);
       } else {
         if (!whole) {
           // ---- owner of a split tile: wait for the other nsegs-1 contributions
           if (lead) {
-            int32_t* cnt = p.counters + tile;
+            int32_t* cnt = p.counters + slot_id;
             int v;
             do {
               asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
@@ -1185,6 +1196,41 @@ static constexpr int ctas_per_sm(int mode, int ntok) { return ntok <= 64 && mode
 #endif
 static constexpr int kPairBk = QQQ_PAIR_BK;
 
+template <int MODE, int NTOK, int BK, bool PAIR>
+__global__ void w4a8_gemm_kernel(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                 const GemmParams);
+
+// 2-CTA clusters of the pair kernel that fit on the GPU at once (a GPC with an
+// odd number of free SMs strands one): the stream-K pair plans never exceed it
+static int pair_slots(int mode) {
+  static int n[2] = {0, 0};
+  const int i = mode == kModePC ? 0 : 1;
+  if (n[i] == 0) {
+    using C = Cfg<kModePG, 256, kPairBk, true>;
+    auto kern = mode == kModePC ? w4a8_gemm_kernel<kModePC, 256, kPairBk, true>
+                                : w4a8_gemm_kernel<kModePG, 256, kPairBk, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(2 * (unsigned)num_sms());
+    lc.blockDim = dim3(C::kNumThreads);
+    lc.dynamicSmemBytes = C::kSmemBytes;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, (void*)kern, &lc) != cudaSuccess || c <= 0) {
+      cudaGetLastError();
+      c = num_sms() / 2 - 4;  // conservative
+    }
+    n[i] = std::min(c, num_sms() / 2);
+  }
+  return n[i];
+}
+
 // split: 0 = whole tiles (data-parallel), 1 = stream-K over all units,
 //        2 = hybrid: full waves of whole tiles, the remainder stream-K'd over all CTAs,
 //        3 = whole 256-channel pair tiles on 2-CTA clusters (NTOK = 256, PC/PG)
@@ -1217,8 +1263,11 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
     lp.grid = lp.tiles * S;
     return lp;
   }
-  if (split == 3 && (ntok != 256 || mode == kModeI8)) split = 0;
-  if (split == 3) {
+  const bool pair_plan = split == 3 || split == 5 || split == 6;
+  if (pair_plan && (ntok != 256 || mode == kModeI8)) split = split == 3 ? 0 : split == 5 ? 1 : 2;
+  if (split == 3 || split == 5 || split == 6) {
+    // pair tiles: 3 = whole pair tiles, 5 = stream-K over (pair tile, k-block) units
+    // across the CTA pairs, 6 = whole-tile waves + the remainder stream-K'd
     lp.ntok = ntok;
     lp.bk = kPairBk;
     lp.pair = 1;
@@ -1228,7 +1277,28 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
     lp.tiles = ((lp.n_tiles + 1) / 2) * lp.tok_tiles;  // pair tiles
     lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
     lp.max_segs = 1;
-    const int pairs = (force_grid > 0 ? std::min(force_grid, num_sms()) : num_sms()) / 2;
+    // co-resident 2-CTA clusters (a split tile's owner waits for its contributors)
+    const int pairs = force_grid > 0 ? std::max(1, std::min(force_grid / 2, pair_slots(mode))) : pair_slots(mode);
+    if (split == 6) {
+      const int waves = lp.tiles / pairs, rem = lp.tiles % pairs;
+      if (waves >= 1 && rem > 0) {
+        lp.grid = 2 * pairs;
+        lp.dp_tiles = waves;
+        lp.sk_unit0 = (int64_t)waves * pairs * lp.kb_per_tile;
+        lp.units = (int64_t)rem * lp.kb_per_tile;
+        const int64_t per = std::max<int64_t>(1, lp.units / pairs);
+        lp.max_segs = (int)std::min<int64_t>((lp.kb_per_tile + per - 1) / per + 1, pairs);
+        return lp;
+      }
+      split = waves >= 1 ? 3 : 5;
+    }
+    if (split == 5) {
+      const int g = (int)std::min<int64_t>(lp.units, pairs);
+      lp.grid = 2 * g;
+      const int64_t per = lp.units / g;
+      lp.max_segs = (int)std::min<int64_t>((lp.kb_per_tile + per - 1) / per + 1, g);
+      return lp;
+    }
     const int per = (lp.tiles + pairs - 1) / pairs;
     lp.aligned_tiles = per;
     lp.grid = 2 * ((lp.tiles + per - 1) / per);
@@ -1351,6 +1421,7 @@ constexpr size_t kCounterBytes = (size_t)kMaxTiles * 4;
 
 static size_t plan_ws_bytes(const LaunchPlan& lp) {
   if (lp.aligned_tiles > 0 || lp.csplit > 1) return kCounterBytes;
+  if (lp.pair) return kCounterBytes + (size_t)lp.tiles * 2 * lp.ntok * 128 * 4;  // a slot per (pair tile, CTA)
   return kCounterBytes + (size_t)lp.tiles * lp.ntok * 128 * 4;
 }
 
@@ -1417,6 +1488,10 @@ extern "C" size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
     size_t b = plan_ws_bytes(lp);
     if (b > best) best = b;
   }
+  {
+    LaunchPlan lp = plan_for(kModePG, M, N, K, 256, 5, 0);  // pair stream-K: a slot per (pair tile, CTA)
+    best = std::max(best, plan_ws_bytes(lp));
+  }
   return best;
 }
 
@@ -1439,7 +1514,7 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   if (!enc) return kErrCuda;
 
   LaunchPlan lp = make_plan(mode, M, N, K, cfg ? cfg->ntok : 0, cfg ? cfg->grid : 0, cfg ? cfg->split : -1);
-  if (lp.tiles > kMaxTiles) return kErrUnsupported;
+  if (lp.tiles * (lp.pair ? 2 : 1) > kMaxTiles) return kErrUnsupported;
   if (ws_bytes < plan_ws_bytes(lp)) return kErrConfig;
 
   CUtensorMap map;

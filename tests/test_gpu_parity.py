@@ -282,8 +282,9 @@ def test_gemm_all_tile_plans(ntok, split):
 
 @pytest.mark.parametrize("scheme,gs", [("per-channel", 0), ("per-group", 128), ("per-group", 32)])
 def test_gemm_pair_tiles(scheme, gs):
-    """2-CTA pair plan (split=3: tcgen05.mma.cta_group::2, 256-channel x 256-token
-    tiles): odd channel-tile counts, ragged tokens, partial last k-block, few pairs."""
+    """2-CTA pair plans (tcgen05.mma.cta_group::2, 256-channel x 256-token tiles):
+    whole tiles, stream-K and hybrid; odd channel-tile counts, ragged tokens,
+    partial last k-block, few pairs."""
     for (m, k, n, grid) in ((77, 2304, 640, 0), (256, 1024, 384, 0), (300, 896, 1024, 0), (600, 1152, 1000, 7),
                             (1, 256, 128, 0), (513, 4096, 256, 4)):
         x16, qw_o = _rand_problem(m, k, n, scheme, gs or 128, seed=m + n)
@@ -293,9 +294,12 @@ def test_gemm_pair_tiles(scheme, gs):
         qw = _to_gpu_qw(qw_o)
         prep = Q.gemm.prepare(qw, Q.FusedScales.from_quantized(qw))
         aq = Q.quant_act_per_token(torch.from_numpy(x16).cuda())
-        out = Q.gemm.run_gemm(aq, prep, n, True, cfg={"ntok": 256, "split": 3, "grid": grid})
-        assert same_bits(out.acc, want.acc), (scheme, gs, m, k, n, grid)
-        assert same_bits(out.y, want.y), (scheme, gs, m, k, n, grid)
+        # 3 = whole pair tiles, 5 = stream-K over pair units, 6 = whole-tile waves + stream-K remainder
+        for split in (3, 5, 6):
+            for _ in range(2):  # the split plans must leave the workspace zeroed for the next launch
+                out = Q.gemm.run_gemm(aq, prep, n, True, cfg={"ntok": 256, "split": split, "grid": grid})
+                assert same_bits(out.acc, want.acc), (scheme, gs, m, k, n, grid, split)
+                assert same_bits(out.y, want.y), (scheme, gs, m, k, n, grid, split)
 
 
 @pytest.mark.parametrize("scheme,gs", [("per-channel", 0), ("per-group", 128), ("per-group", 32)])
