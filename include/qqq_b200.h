@@ -156,7 +156,10 @@ int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const int
 typedef struct qqq_gemm_config {
   int ntok;  /* tokens per UMMA tile: 16/32/64/128/256, 0 = auto */
   int grid;  /* CTAs for stream-K, 0 = auto */
-  int split; /* -1 auto, 0 whole tiles, 1 stream-K, 2 whole-tile waves + stream-K remainder */
+  int split; /* -1 auto, 0 whole tiles, 1 stream-K, 2 whole-tile waves + stream-K remainder,
+              * 3 whole 256x256 pair tiles (2-CTA clusters, ntok 256), 4 cluster split-K
+              * (ntok 16/32: one tile per cluster, DSMEM reduction), 5 stream-K over pair
+              * tiles, 6 pair-tile waves + stream-K remainder */
   void* dbg; /* optional device buffer [grid][64] u64: per-CTA %globaltimer timeline (diagnostics) */
 } qqq_gemm_config;
 
