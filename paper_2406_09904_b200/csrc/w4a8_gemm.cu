@@ -1241,8 +1241,8 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
   // the exchange ran at ~7 B/clk per SM.)
   if (split == 4 && (ntok > 32 || ctas_per_sm(mode, ntok) != 2)) split = 1;
   if (split == 4) {
-    // cluster split-K: one tile per cluster of S decode CTAs, S in {8, 4, 2}: the
-    // largest that fits the CTA slots and leaves every rank >= 1 k-block
+    // cluster split-K: one tile per cluster of S decode CTAs: the largest S that
+    // fits the CTA slots and leaves every rank >= 1 k-block
     lp.ntok = ntok;
     lp.bk = bk_for(mode, ntok);
     lp.tok_tiles = (int)((M + ntok - 1) / ntok);
@@ -1252,12 +1252,22 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
     lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
     lp.max_segs = 1;
     const int slots = (force_grid > 0 ? std::min(force_grid, num_sms()) : num_sms()) * ctas_per_sm(mode, ntok);
+    // Cluster size S <= 8 (portable), receive buffer [S][ceil(128/S)][NTOK] int32
+    // within the 16 KiB partial ring (every S for NTOK=16, divisors of 128 for
+    // 32). Measured (profiles/r01_csplit_size_sweep.txt): the fastest S is the
+    // smallest that keeps >= 0.8 CTAs per SM pulling weights and <= 8 k-blocks per
+    // CTA — more, shorter CTAs lose to SM sharing and per-CTA fixed costs (4096x4096:
+    // S=4 5.6 us vs S=8 7.9 us), fewer, longer ones to the per-CTA stream rate.
+    auto fits = [&](int c) {
+      const int rows_per = (128 + c - 1) / c;
+      return (int64_t)lp.tiles * c <= slots && c <= lp.kb_per_tile && c * rows_per * ntok * 4 <= 16384;
+    };
     int S = 1;
-    for (int c : {8, 4, 2})
-      if ((int64_t)lp.tiles * c <= slots && c <= lp.kb_per_tile) {
-        S = c;
-        break;
-      }
+    for (int c = 2; c <= 8; ++c) {
+      if (!fits(c)) continue;
+      S = c;  // the largest fitting S, unless a smaller one meets both targets below
+      if (lp.tiles * c * 5 >= num_sms() * 4 && (lp.kb_per_tile + c - 1) / c <= 8) break;
+    }
     if (S == 1) return plan_for(mode, M, N, K, ntok, 1, force_grid);
     lp.csplit = S;
     lp.grid = lp.tiles * S;
@@ -1368,12 +1378,12 @@ static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
   const double mt = (double)std::min<int64_t>(lp.ntok, M) / 16.0;
   const double epi = kE0 + kE1 * mt;
   if (lp.csplit > 1) {
-    // cluster split-K (linear fit to profiles/r01_decode_sweep.jsonl, 7% rms): a
-    // fixed cost, the per-CTA k-blocks scaled by the CTA-slot occupancy (the
-    // decode stream shares HBM), +2.4 us for the 32-token tile (2 weight stages)
+    // cluster split-K (linear fit to profiles/r01_csplit_sweep.jsonl, 7% rms): a
+    // fixed cost, the per-CTA k-blocks, a penalty for the k-blocks of CTAs that
+    // share an SM, +2.2 us for the 32-token tile (2 weight stages)
     const int ucta_cs = (lp.kb_per_tile + lp.csplit - 1) / lp.csplit;
-    const double occ = (double)lp.grid / (num_sms() * 2);
-    return 5.138 + 1.079 * occ * ucta_cs + (lp.ntok == 32 ? 2.412 : 0.0) + 0.051 * mt;
+    const double shared = std::max(0, lp.grid - num_sms()) / (double)num_sms();
+    return 4.813 + 0.456 * ucta_cs + 0.671 * shared * ucta_cs + (lp.ntok == 32 ? 2.229 : 0.0) + 0.012 * mt;
   }
   if (lp.pair) {
     // 2-CTA pair tiles: ~0.41 us per 128-deep k-block of a 256x256 pair tile

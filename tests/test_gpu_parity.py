@@ -308,7 +308,7 @@ def test_gemm_cluster_splitk(scheme, gs, ntok):
     """Cluster split-K plan (split=4): one tile per cluster of S in {8, 4, 2} decode
     CTAs, int32 partials reduce-scattered over DSMEM; ragged M, partial last k-block."""
     for (m, k, n) in ((1, 4096, 4096), (16, 2048, 11008), (5, 1024, 640), (31, 2304, 384), (13, 4352, 256),
-                      (100, 4096, 4096), (128, 1024, 1280)):
+                      (100, 4096, 4096), (128, 1024, 1280), (3, 4096, 11008), (2, 1792, 5376), (4, 2560, 7552)):
         x16, qw_o = _rand_problem(m, k, n, scheme, gs or 128, seed=m * 7 + n)
         aq_o = O.quant_act_per_token(x16.astype(np.float64))
         run_o = O.w4a8_gemm_per_channel if scheme == "per-channel" else O.w4a8_gemm_per_group
