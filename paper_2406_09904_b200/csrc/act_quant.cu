@@ -505,11 +505,14 @@ static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, in
   lc.attrs = attr;
   lc.numAttrs = 1;
   cudaError_t e;
-  // small M (decode batches), smoothed fp16 rows up to 8 x 256 vectors: row split over
+  // M <= 256 (decode and mid batches), smoothed fp16 rows up to 8 x 256 vectors: row split over
   // a cluster (measured: 4.7 vs 5.2 us per smoothed M=1 quantizer in the C4 chain; the
   // plain quantizer's ~35 instructions per element gain nothing from it)
   constexpr int kCT = 256;
-  if (smooth && x_dtype == 0 && !row_max_in && !row_max_out && !smooth_mask && M <= 64 && K % 8 == 0 &&
+#ifndef QQQ_QCLUSTER_MAXM
+#define QQQ_QCLUSTER_MAXM 256
+#endif
+  if (smooth && x_dtype == 0 && !row_max_in && !row_max_out && !smooth_mask && M <= QQQ_QCLUSTER_MAXM && K % 8 == 0 &&
       K <= (int64_t)8 * kCT * 8 && ldx % 8 == 0 && ldq % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(q) & 7) == 0 && (reinterpret_cast<uintptr_t>(smooth) & 15) == 0) {
     const int G = (int)((K / 8 + kCT - 1) / kCT);
