@@ -322,6 +322,32 @@ def test_gemm_cluster_splitk(scheme, gs, ntok):
             assert same_bits(out.y, want.y), (scheme, gs, ntok, m, k, n)
 
 
+def test_gemm_plans_share_a_zeroed_workspace():
+    """Every plan leaves the shared split-K workspace zeroed (counters re-armed,
+    slots returned to zero): a chain of GEMMs of different shapes and plans —
+    stream-K, hybrid, pair stream-K, cluster split-K — on ONE workspace stays
+    bit-exact, twice over."""
+    cases = [((128, 4096, 512), {"ntok": 128, "split": 1}), ((77, 2304, 640), {"ntok": 128, "split": 2}),
+             ((300, 1024, 1024), {"ntok": 256, "split": 5}), ((16, 4096, 4096), {"ntok": 16, "split": 1}),
+             ((5, 2048, 1280), {"ntok": 16, "split": 4}), ((600, 1152, 1000), {"ntok": 256, "split": 6})]
+    import paper_2406_09904_b200._lib as L
+    need = max(L.load().qqq_gemm_workspace_bytes(m, n, k) for (m, k, n), _ in cases)
+    ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+    for rep in range(2):
+        for (m, k, n), cfg in cases:
+            x16, qw_o = _rand_problem(m, k, n, "per-group", 128, seed=m + k + n + rep)
+            aq_o = O.quant_act_per_token(x16.astype(np.float64))
+            want = O.w4a8_gemm_per_group(aq_o, qw_o, O.FusedScales.from_quantized(qw_o), fast=True)
+            qw = _to_gpu_qw(qw_o)
+            prep = Q.gemm.prepare(qw, Q.FusedScales.from_quantized(qw))
+            aq = Q.quant_act_per_token(torch.from_numpy(x16).cuda())
+            out = Q.gemm.run_gemm(aq, prep, n, True, cfg=cfg, ws=ws)
+            assert same_bits(out.acc, want.acc), (m, k, n, cfg, rep)
+            assert same_bits(out.y, want.y), (m, k, n, cfg, rep)
+    torch.cuda.synchronize()
+    assert int(ws.count_nonzero()) == 0  # counters re-armed, every slot returned to zero
+
+
 def test_gemm_ragged_shapes():
     for (m, k, n, scheme, gs) in ((3, 33, 5, "per-channel", 0), (9, 100, 130, "per-channel", 0),
                                   (4, 96, 129, "per-group", 32), (2, 300, 1, "per-group", 100)):
