@@ -68,6 +68,18 @@ int qqq_act_quant_ex(const void* x, int x_dtype, int64_t M, int64_t K, int64_t l
 int qqq_act_quant_smooth(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, const double* smooth,
                          const uint8_t* smooth_mask, int8_t* q, int64_t ldq, double* s_a, int32_t* rowsum,
                          int32_t* status_dev, qqq_stream_t stream);
+/* Reciprocal table of a smoothing vector (once per layer): recip[k] = RN(1/smooth[k])
+ * (IEEE division), NaN where |smooth[k]| is outside [2^-400, 2^400]. */
+int qqq_smooth_reciprocal(const double* smooth, int64_t K, double* recip, qqq_stream_t stream);
+/* qqq_act_quant_smooth with that table: each x / smooth[k] is computed as a
+ * Markstein FMA sequence from recip[k] (the same correctly rounded quotient, so
+ * codes and scales stay bit-identical to pipeline.py:146 + quantize.py:92-100);
+ * NaN entries keep the IEEE division. The table is read for M <= 32 (decode
+ * batches, where it measured faster); larger batches divide as
+ * qqq_act_quant_smooth does. */
+int qqq_act_quant_smooth_rcp(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, const double* smooth,
+                             const double* smooth_recip, int8_t* q, int64_t ldq, double* s_a, int32_t* rowsum,
+                             int32_t* status_dev, qqq_stream_t stream);
 /* rowsum of existing int8 codes (activations not produced by qqq_act_quant_ex). */
 int qqq_act_rowsum(const int8_t* q, int64_t M, int64_t K, int64_t ldq, int32_t* rowsum, qqq_stream_t stream);
 

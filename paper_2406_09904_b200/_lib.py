@@ -37,6 +37,8 @@ SIGNATURES = {
     "qqq_act_quant_ex": (c_int, [P, c_int, I64, I64, I64, P, I64, P, P, P, S]),
     "qqq_act_rowsum": (c_int, [P, I64, I64, I64, P, S]),
     "qqq_act_quant_smooth": (c_int, [P, c_int, I64, I64, I64, P, P, P, I64, P, P, P, S]),
+    "qqq_smooth_reciprocal": (c_int, [P, I64, P, S]),
+    "qqq_act_quant_smooth_rcp": (c_int, [P, c_int, I64, I64, I64, P, P, P, I64, P, P, P, S]),
     "qqq_act_absmax": (c_int, [P, c_int, I64, I64, I64, P, P, S]),
     "qqq_act_quant_with_max": (c_int, [P, c_int, I64, I64, I64, P, P, I64, P, P, P, S]),
     "qqq_dequant_epilogue": (c_int, [P, I64, I64, I64, P, P, P, I64, S]),

@@ -56,6 +56,114 @@ QQQ_DEVICE int8_t quant_code_f64(double x, double inv, double s) {
 // channels are not smoothed (s_k == 1.0, x / 1.0 == x exactly)
 QQQ_DEVICE double smooth_div(double x, double sk) { return sk == 1.0 ? x : x / sk; }
 
+// RN(a / b) without the division routine (Markstein): y = RN(1/b); q0 =
+// RN(a*y) can be ~1.3 ulp off, so one FMA correction q1 = RN(q0 + RN(a - b*q0)*y)
+// brings it within one ulp; then r1 = a - b*q1 is exact in one FMA and
+// RN(q1 + r1*y) is the correctly rounded quotient (Markstein's theorem, y within
+// half an ulp of 1/b), i.e. the IEEE division numpy performs. The callers keep
+// |b| and the quotients inside the normal range (qqq_smooth_reciprocal). b == 1
+// gives a exactly (y = 1, residuals 0). Checked in exact rational arithmetic by
+// tests/test_pipeline.py::test_markstein_division_is_ieee.
+QQQ_DEVICE double div_markstein(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double q1 = __fma_rn(__fma_rn(-q0, b, a), y, q0);
+  return __fma_rn(__fma_rn(-q1, b, a), y, q1);
+}
+
+// 8 int8 codes (low byte of each word) -> 8 packed bytes; csum += their sum
+QQQ_DEVICE uint2 pack8(const uint32_t (&b)[8], int& csum) {
+  uint2 o;
+  o.x = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+  o.y = __byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410);
+  csum = __dp4a((int)o.x, 0x01010101, csum);
+  csum = __dp4a((int)o.y, 0x01010101, csum);
+  return o;
+}
+
+// Codes of 8 fp16 values (quantize.py:99 rint(x / s), clip): t = x * RN(127/m)
+// in fp32, rounded half-even by adding 1.5*2^23 (the code is then the low byte
+// of the sum's bits; |t| <= 127 < 2^22). One batched test per 8 values: if any
+// t lies within 2^-14 of a half-integer, all 8 take the reference formula in
+// f64. The band: inv = 127/m (1 + d1), t = x*inv (1 + d2), |d1|, |d2| <= 2^-24,
+// so |t - x*127/m| <= 127 * 2.01 * 2^-24 < 1.6e-5 < 2^-14 = 6.1e-5 (and the
+// reference quotient is within 2^-44 of x*127/m). A wider band (1e-3, as in
+// quant_code_f16) sent ~40% of the warps of a K=11008 row into the f64 path.
+QQQ_DEVICE uint2 codes8_f16(const uint4& v, float inv, double s, double rs, int& csum) {
+  constexpr float kMagic = 12582912.0f;
+  const __half* e = reinterpret_cast<const __half*>(&v);
+  uint32_t b[8];
+  float emax = 0.0f;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const float tt = __fmul_rn(__half2float(e[t]), inv);
+    const float w = __fadd_rn(tt, kMagic);
+    emax = fmaxf(emax, fabsf(__fsub_rn(tt, __fsub_rn(w, kMagic))));
+    b[t] = __float_as_uint(w);
+  }
+  if (emax > 0.5f - 0x1p-14f) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t)  // rint(RN(x / s)) exactly (s = m/127 with m an fp16 value: Markstein-safe)
+      b[t] = (uint32_t)__double2loint(__dadd_rn(div_markstein((double)__half2float(e[t]), s, rs), 6755399441055744.0));
+  }
+  return pack8(b, csum);
+}
+
+// Codes of 8 smoothed f64 values: u = RN(x / s) by Markstein (rs = RN(1/s)),
+// rint(u) half-even by adding 1.5*2^52 (|u| <= 127, no clip needed since
+// |x| <= m). Bit-identical to the reference, no near-tie fallback. `ieee`:
+// s outside the range where the FMA residual stays normal -> IEEE division.
+QQQ_DEVICE uint2 codes8_f64(const double (&xs)[8], double s, double rs, bool ieee, int& csum) {
+  constexpr double kMagic = 6755399441055744.0;
+  uint32_t b[8];
+  if (ieee) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) b[t] = (uint32_t)(int)quant_code_exact(xs[t], s);
+  } else {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) b[t] = (uint32_t)__double2loint(__dadd_rn(div_markstein(xs[t], s, rs), kMagic));
+  }
+  return pack8(b, csum);
+}
+
+// x / s_k for the 8 channels of one vector (pipeline.py:146): with the
+// reciprocal table y (qqq_smooth_reciprocal; NaN marks a channel whose s_k is
+// outside the safe range) by Markstein, else IEEE division
+QQQ_DEVICE void smooth8(const uint4& v, const double* __restrict__ smooth, const double* __restrict__ recip,
+                        int64_t i, double (&xs)[8]) {
+  const __half* e = reinterpret_cast<const __half*>(&v);
+  const double2* sv = reinterpret_cast<const double2*>(smooth + i * 8);
+  double sk[8];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const double2 d = __ldg(sv + h);
+    sk[2 * h] = d.x;
+    sk[2 * h + 1] = d.y;
+  }
+  bool slow = recip == nullptr;
+  if (!slow) {
+    const double2* yv = reinterpret_cast<const double2*>(recip + i * 8);
+    double y[8];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const double2 d = __ldg(yv + h);
+      y[2 * h] = d.x;
+      y[2 * h + 1] = d.y;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      xs[t] = div_markstein((double)__half2float(e[t]), sk[t], y[t]);
+      slow |= y[t] != y[t];
+    }
+  }
+  if (slow) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) xs[t] = (double)__half2float(e[t]) / sk[t];
+  }
+}
+
+// Markstein is exact while the quotients and FMA residuals stay normal
+QQQ_DEVICE bool markstein_safe(double b) { return fabs(b) >= 0x1p-400 && fabs(b) <= 0x1p400; }
+
 // fp16 fast path; inv = RN(127/m) in fp32 (m = row absmax > 0), s the f64
 // scale. |x*inv - x*127/m| <= 2*127*2^-24 < 2e-5, far inside the 1e-3 band.
 QQQ_DEVICE int8_t quant_code_f16(float x, float inv, double s) {
@@ -216,7 +324,8 @@ __global__ void __launch_bounds__(kThreads) act_quant_row_kernel(const __half* _
                                                                   double* __restrict__ s_out, int32_t* status,
                                                                   int32_t* __restrict__ rowsum_out,
                                                                   const double* __restrict__ smooth,
-                                                                  const uint8_t* __restrict__ smooth_mask) {
+                                                                  const uint8_t* __restrict__ smooth_mask,
+                                                                  const double* __restrict__ recip) {
   using Acc = typename std::conditional<kSmooth, double, float>::type;
   __shared__ Acc red[32];
   __shared__ int isum[kThreads / 32];
@@ -259,6 +368,16 @@ __global__ void __launch_bounds__(kThreads) act_quant_row_kernel(const __half* _
     if (i < nv) {
       const __half* e = reinterpret_cast<const __half*>(&v[j]);
       if constexpr (kSmooth) {
+        if (recip != nullptr) {  // Markstein division with the reciprocal table
+          smooth8(v[j], smooth, recip, i, xs[j]);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const Acc a = fabs(xs[j][t]);
+            bad |= is_bad(a);
+            m = a > m ? a : m;
+          }
+          continue;
+        }
         double sk[8];
         if (smooth_mask == nullptr) {
           const double2* sv = reinterpret_cast<const double2*>(smooth + i * 8);  // 64 B per vector
@@ -295,29 +414,20 @@ __global__ void __launch_bounds__(kThreads) act_quant_row_kernel(const __half* _
   if (threadIdx.x == 0) s_out[row] = s;
   const bool zero_row = !(m > Acc(0));
   const float inv = zero_row ? 0.0f : 127.0f / (float)m;
-  const double inv64 = 1.0 / s;
+  const double rs = 1.0 / s;
+  const bool ieee = !markstein_safe(s);
   int8_t* qr = q + row * ldq;
   int csum = 0;
 #pragma unroll
   for (int j = 0; j < kVPT; ++j) {
     const int64_t i = threadIdx.x + (int64_t)j * kThreads;
     if (i < nv) {
-      const __half* e = reinterpret_cast<const __half*>(&v[j]);
-      alignas(8) int8_t out[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        int8_t c = 0;
-        if (!zero_row) {
-          if constexpr (kSmooth) {
-            c = quant_code_f64(xs[j][t], inv64, s);
-          } else {
-            c = quant_code_f16(__half2float(e[t]), inv, s);
-          }
-        }
-        out[t] = c;
-        csum += c;
-      }
-      *reinterpret_cast<uint2*>(qr + i * 8) = *reinterpret_cast<const uint2*>(out);
+      uint2 o;
+      if constexpr (kSmooth)
+        o = codes8_f64(xs[j], s, rs, ieee, csum);
+      else
+        o = codes8_f16(v[j], inv, s, rs, csum);
+      *reinterpret_cast<uint2*>(qr + i * 8) = o;
     }
   }
   if (rowsum_out) {
@@ -360,7 +470,8 @@ __global__ void __launch_bounds__(kThreads) act_quant_cluster_kernel(const __hal
                                                                       int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
                                                                       double* __restrict__ s_out, int32_t* status,
                                                                       int32_t* __restrict__ rowsum_out,
-                                                                      const double* __restrict__ smooth) {
+                                                                      const double* __restrict__ smooth,
+                                                                      const double* __restrict__ recip) {
   using Acc = typename std::conditional<kSmooth, double, float>::type;
   __shared__ uint64_t bar[2];       // [0] peer maxima landed, [1] (rank 0) peer code sums landed
   __shared__ double peer_max[8];
@@ -382,30 +493,21 @@ __global__ void __launch_bounds__(kThreads) act_quant_cluster_kernel(const __hal
   const int64_t i = v0 + threadIdx.x;
   const bool has = i < v1;
   uint4 v = has ? __ldg(reinterpret_cast<const uint4*>(x + row * ldx) + i) : make_uint4(0, 0, 0, 0);
-  double sk[8];
+  const __half* e = reinterpret_cast<const __half*>(&v);
+  double xs[8];
   if constexpr (kSmooth) {
     if (has) {
-      const double2* sv = reinterpret_cast<const double2*>(smooth + i * 8);
+      smooth8(v, smooth, recip, i, xs);
+    } else {
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const double2 d = __ldg(sv + h);
-        sk[2 * h] = d.x;
-        sk[2 * h + 1] = d.y;
-      }
+      for (int t = 0; t < 8; ++t) xs[t] = 0.0;
     }
   }
-  const __half* e = reinterpret_cast<const __half*>(&v);
-  Acc xs[8];
   Acc m = Acc(0);
   bool bad = false;
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
-    if constexpr (kSmooth) {
-      xs[t] = has ? (double)__half2float(e[t]) / sk[t] : 0.0;
-    } else {
-      xs[t] = __half2float(e[t]);
-    }
-    const Acc a = fabs(xs[t]);
+    const Acc a = kSmooth ? (Acc)fabs(xs[t]) : (Acc)fabsf(__half2float(e[t]));
     bad |= is_bad(a);
     m = a > m ? a : m;
   }
@@ -430,23 +532,15 @@ __global__ void __launch_bounds__(kThreads) act_quant_cluster_kernel(const __hal
   const double s = (mr > Acc(0)) ? (double)mr / 127.0 : 1.0;
   const bool zero_row = !(mr > Acc(0));
   const float inv = zero_row ? 0.0f : 127.0f / (float)mr;
-  const double inv64 = 1.0 / s;
+  const double rs = 1.0 / s;
   int csum = 0;
   if (has) {
-    alignas(8) int8_t out[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      int8_t c = 0;
-      if (!zero_row) {
-        if constexpr (kSmooth)
-          c = quant_code_f64(xs[t], inv64, s);
-        else
-          c = quant_code_f16(xs[t], inv, s);
-      }
-      out[t] = c;
-      csum += c;
-    }
-    *reinterpret_cast<uint2*>(q + row * ldq + i * 8) = *reinterpret_cast<const uint2*>(out);
+    uint2 o;
+    if constexpr (kSmooth)
+      o = codes8_f64(xs, s, rs, !markstein_safe(s), csum);
+    else
+      o = codes8_f16(v, inv, s, rs, csum);
+    *reinterpret_cast<uint2*>(q + row * ldq + i * 8) = o;
   }
   for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
   if ((threadIdx.x & 31) == 0) isum[threadIdx.x >> 5] = csum;
@@ -491,7 +585,7 @@ using namespace qqq;
 static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx, int8_t* q, int64_t ldq,
                             double* s_a, int32_t* status_dev, const double* row_max_in, double* row_max_out,
                             int32_t* rowsum, cudaStream_t stream, const double* smooth = nullptr,
-                            const uint8_t* smooth_mask = nullptr) {
+                            const uint8_t* smooth_mask = nullptr, const double* recip = nullptr) {
   if (M < 0 || K <= 0 || ldx < K || (!row_max_out && ldq < K)) return kErrShape;
   if (M == 0) return kOk;
   constexpr int kT = 256;
@@ -509,12 +603,18 @@ static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, in
   // a cluster (measured: 4.7 vs 5.2 us per smoothed M=1 quantizer in the C4 chain; the
   // plain quantizer's ~35 instructions per element gain nothing from it)
   constexpr int kCT = 256;
+  // The reciprocal table replaces the per-element division routine by 5 FMA-pipe
+  // ops but adds a 64-byte table read per 8 channels: a win for decode batches
+  // (C4 stack quantizers 16.5 -> 14.7 us at M = 1..16), a loss from M ~ 64 on
+  // (33.0 -> 36.9 us at M = 256), where the kernel waits on loads, not issue.
+  constexpr int64_t kRecipMaxM = 32;
 #ifndef QQQ_QCLUSTER_MAXM
 #define QQQ_QCLUSTER_MAXM 256
 #endif
   if (smooth && x_dtype == 0 && !row_max_in && !row_max_out && !smooth_mask && M <= QQQ_QCLUSTER_MAXM && K % 8 == 0 &&
       K <= (int64_t)8 * kCT * 8 && ldx % 8 == 0 && ldq % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
-      (reinterpret_cast<uintptr_t>(q) & 7) == 0 && (reinterpret_cast<uintptr_t>(smooth) & 15) == 0) {
+      (reinterpret_cast<uintptr_t>(q) & 7) == 0 && (reinterpret_cast<uintptr_t>(smooth) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(recip) & 15) == 0) {
     const int G = (int)((K / 8 + kCT - 1) / kCT);
     cudaLaunchAttribute ca[2];
     ca[0] = attr[0];
@@ -528,7 +628,7 @@ static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, in
     cc.attrs = ca;
     cc.numAttrs = 2;
     e = cudaLaunchKernelEx(&cc, act_quant_cluster_kernel<kCT, true>, (const __half*)x, K, ldx, q, ldq, s_a,
-                           status_dev, rowsum, smooth);
+                           status_dev, rowsum, smooth, M <= kRecipMaxM ? recip : nullptr);
     return e == cudaSuccess ? kOk : kErrCuda;
   }
   // fp16 rows that fit one CTA's registers: the single-round-trip kernel
@@ -536,14 +636,15 @@ static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, in
   if (x_dtype == 0 && !row_max_in && !row_max_out && K % 8 == 0 &&
       K <= (int64_t)kRT * kRV * 8 && ldx % 8 == 0 &&
       ldq % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(q) & 7) == 0 &&
-      (reinterpret_cast<uintptr_t>(smooth) & 15) == 0) {  // (smoothing vector read as 16-byte pairs)
+      (reinterpret_cast<uintptr_t>(smooth) & 15) == 0 &&  // (smoothing vector read as 16-byte pairs)
+      (reinterpret_cast<uintptr_t>(recip) & 15) == 0) {
     lc.blockDim = dim3(kRT);
     if (smooth)
       e = cudaLaunchKernelEx(&lc, act_quant_row_kernel<kRT, kRV, true>, (const __half*)x, K, ldx, q, ldq, s_a,
-                             status_dev, rowsum, smooth, smooth_mask);
+                             status_dev, rowsum, smooth, smooth_mask, M <= kRecipMaxM ? recip : nullptr);
     else
       e = cudaLaunchKernelEx(&lc, act_quant_row_kernel<kRT, kRV, false>, (const __half*)x, K, ldx, q, ldq, s_a,
-                             status_dev, rowsum, smooth, smooth_mask);
+                             status_dev, rowsum, smooth, smooth_mask, (const double*)nullptr);
     return e == cudaSuccess ? kOk : kErrCuda;
   }
   if (smooth) {
@@ -623,4 +724,33 @@ extern "C" int qqq_act_quant_smooth(const void* x, int x_dtype, int64_t M, int64
   if (!smooth) return kErrConfig;
   return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, nullptr, nullptr, rowsum, stream, smooth,
                           smooth_mask);
+}
+
+// Reciprocal table of a smoothing vector for qqq_act_quant_smooth_rcp:
+// recip[k] = RN(1/s_k) (IEEE division), or NaN where 2^-400 <= |s_k| <= 2^400
+// does not hold (those channels keep the IEEE division of x / s_k).
+__global__ void smooth_recip_kernel(const double* __restrict__ smooth, int64_t K, double* __restrict__ recip) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < K) {
+    const double b = smooth[k];
+    recip[k] = markstein_safe(b) ? 1.0 / b : __longlong_as_double(0x7ff8000000000000LL);
+  }
+}
+
+extern "C" int qqq_smooth_reciprocal(const double* smooth, int64_t K, double* recip, cudaStream_t stream) {
+  if (!smooth || !recip) return kErrConfig;
+  if (K <= 0) return kErrShape;
+  smooth_recip_kernel<<<(unsigned)((K + 255) / 256), 256, 0, stream>>>(smooth, K, recip);
+  return cudaGetLastError() == cudaSuccess ? kOk : kErrCuda;
+}
+
+// qqq_act_quant_smooth with the smoothing vector's reciprocal table: the x / s_k
+// divisions become Markstein FMA sequences (same IEEE quotients, bit-identical
+// codes and scales), the form a layer uses once its table is cached.
+extern "C" int qqq_act_quant_smooth_rcp(const void* x, int x_dtype, int64_t M, int64_t K, int64_t ldx,
+                                        const double* smooth, const double* smooth_recip, int8_t* q, int64_t ldq,
+                                        double* s_a, int32_t* rowsum, int32_t* status_dev, cudaStream_t stream) {
+  if (!smooth || !smooth_recip) return kErrConfig;
+  return act_quant_launch(x, x_dtype, M, K, ldx, q, ldq, s_a, status_dev, nullptr, nullptr, rowsum, stream, smooth,
+                          nullptr, smooth_recip);
 }

@@ -25,7 +25,8 @@ from .gemm import FusedScales, w4a8_gemm_per_channel, w4a8_gemm_per_group
 from .quantize import (PER_CHANNEL, QuantizedActivations, QuantizedWeights, as_cuda, attach_rowsum, deferred_status,
                        raise_if_bad)
 
-__all__ = ["SmoothingPlan", "QuantizedLayer", "identity_plan", "quant_act_smoothed", "apply_quant_linear"]
+__all__ = ["SmoothingPlan", "QuantizedLayer", "identity_plan", "smoothing_reciprocal", "quant_act_smoothed",
+           "apply_quant_linear"]
 
 
 @dataclass(frozen=True)
@@ -52,9 +53,25 @@ class QuantizedLayer:  # pipeline.py:86-90
     _cache: dict = field(default_factory=dict, repr=False, compare=False)
 
 
-def quant_act_smoothed(x, s, check: bool = True) -> QuantizedActivations:
+def smoothing_reciprocal(s) -> torch.Tensor:
+    """Device table RN(1/s_k) (NaN where |s_k| is outside [2^-400, 2^400]) for
+    quant_act_smoothed(..., recip=): computed once per smoothing vector."""
+    st = as_cuda(s if isinstance(s, torch.Tensor) else np.asarray(s, dtype=np.float64), torch.float64).contiguous()
+    if st.ndim != 1:
+        raise ShapeError("smoothing vector must be 1-D")
+    out = torch.empty_like(st)
+    if st.numel():
+        _lib.check(_lib.lib_for_device(st.device).qqq_smooth_reciprocal(_lib.ptr(st), st.numel(), _lib.ptr(out),
+                                                                        _lib.stream_of(st.device)),
+                   "smoothing_reciprocal")
+    return out
+
+
+def quant_act_smoothed(x, s, check: bool = True, recip: torch.Tensor = None) -> QuantizedActivations:
     """quant_act_per_token(x / s) with the f64 divide fused into the quantizer
-    (pipeline.py:146): bit-identical codes and scales to the reference."""
+    (pipeline.py:146): bit-identical codes and scales to the reference. With
+    `recip` (smoothing_reciprocal(s)) the divisions run as Markstein FMA
+    sequences — the same IEEE quotients at a fraction of the instructions."""
     xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64)))
     if xt.ndim != 2:
         raise ShapeError("activations must be 2-D (tokens x K)")
@@ -79,10 +96,16 @@ def quant_act_smoothed(x, s, check: bool = True) -> QuantizedActivations:
         ldx = xt.stride(0) if m > 1 else k
         # (no channel mask: with ~1/8 smoothed channels every warp diverges into the
         # division anyway, and the mask loads measured slower)
-        _lib.check(lib.qqq_act_quant_smooth(_lib.ptr(xt), dt, m, k, ldx, _lib.ptr(st), None,
-                                            _lib.ptr(qbuf), kp,
-                                            _lib.ptr(s_a), _lib.ptr(rowsum), _lib.ptr(status), _lib.stream_of(dev)),
-                   "quant_act_smoothed")
+        if recip is not None:
+            if tuple(recip.shape) != (k,) or recip.dtype != torch.float64 or recip.device != dev:
+                raise ShapeError("recip must be smoothing_reciprocal(s) on the activations' device")
+            rc = lib.qqq_act_quant_smooth_rcp(_lib.ptr(xt), dt, m, k, ldx, _lib.ptr(st), _lib.ptr(recip.contiguous()),
+                                              _lib.ptr(qbuf), kp, _lib.ptr(s_a), _lib.ptr(rowsum), _lib.ptr(status),
+                                              _lib.stream_of(dev))
+        else:
+            rc = lib.qqq_act_quant_smooth(_lib.ptr(xt), dt, m, k, ldx, _lib.ptr(st), None, _lib.ptr(qbuf), kp,
+                                          _lib.ptr(s_a), _lib.ptr(rowsum), _lib.ptr(status), _lib.stream_of(dev))
+        _lib.check(rc, "quant_act_smoothed")
     out = QuantizedActivations(q=qbuf[:, :k], s_a=s_a)
     attach_rowsum(out, rowsum)
     if check:
@@ -95,7 +118,10 @@ def quant_act_smoothed(x, s, check: bool = True) -> QuantizedActivations:
 def apply_quant_linear(x, layer: QuantizedLayer, check: bool = True) -> torch.Tensor:
     """Quantized forward of one linear (pipeline.py:144-152): divide by s,
     quantize, W4A8 GEMM; returns y widened to f64 (GemmOutput.y_wide)."""
-    qa = quant_act_smoothed(x, layer.plan.s, check=check)
+    recip = layer._cache.get("recip")
+    if recip is None:  # the plan's reciprocal table, once per layer
+        recip = layer._cache["recip"] = smoothing_reciprocal(layer.plan.s)
+    qa = quant_act_smoothed(x, layer.plan.s, check=check, recip=recip)
     fused = layer._cache.get("fused")
     if fused is None:  # the reference rebuilds FusedScales per call; it is a pure function of the weights
         fused = FusedScales.from_quantized(layer.qweights)

@@ -98,3 +98,68 @@ def test_gpu_quant_act_smoothed_random_vs_oracle(k):
         got = Q.quant_act_smoothed(torch.from_numpy(x16).cuda(), s)
         assert np.array_equal(got.q.cpu().numpy(), want.q), (k, m)
         assert np.array_equal(got.s_a.cpu().numpy().view(np.uint64), want.s_a.view(np.uint64)), (k, m)
+
+
+def _markstein(a: float, b: float) -> float:
+    """The kernel's division (act_quant.cu div_markstein) in exact rational
+    arithmetic (float(Fraction) rounds to nearest even, like each FMA):
+    y = RN(1/b), q0 = RN(a*y), q1 = fma(fma(-q0, b, a), y, q0),
+    result = fma(fma(-q1, b, a), y, q1)."""
+    from fractions import Fraction as F
+
+    y = 1.0 / b
+    q0 = a * y
+    q1 = float(F(q0) + F(float(F(a) - F(q0) * F(b))) * F(y))
+    r_exact = F(a) - F(q1) * F(b)
+    r = float(r_exact)
+    assert F(r) == r_exact  # q1 is within one ulp: the residual is exact (Markstein)
+    return float(F(q1) + F(r) * F(y))
+
+
+def test_markstein_division_is_ieee():
+    """x / s_k and x / s as Markstein FMA sequences equal numpy's IEEE division:
+    fp16 numerators against smoothing factors, and f64 numerators against
+    per-token scales, at the magnitudes the quantizer admits."""
+    rng = np.random.default_rng(7)
+    f16 = np.arange(0, 0x7C00, dtype=np.uint16).view(np.float16).astype(np.float64)
+    a = np.concatenate([f16[rng.integers(0, f16.size, 6000)], -f16[rng.integers(0, f16.size, 2000)],
+                        rng.standard_normal(4000) * 10.0 ** rng.uniform(-30, 30, 4000)])
+    b = np.concatenate([rng.uniform(0.05, 20.0, 4000), 10.0 ** rng.uniform(-100, 100, 4000),
+                        rng.uniform(1e-3, 1.0, 4000) / 127.0])
+    b[:50] = 1.0
+    b[50:100] = np.nextafter(1.0, 2.0) * np.arange(1, 51)
+    for ai, bi in zip(a.tolist(), b.tolist()):
+        assert _markstein(ai, bi) == ai / bi, (ai, bi)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [4096, 11008])
+def test_gpu_quant_act_smoothed_recip_vs_oracle(k):
+    """The reciprocal-table (Markstein) quantizer: cluster rows (M <= 256) and
+    register rows (M > 256), every finite fp16 value present, unsafe smoothing
+    factors (NaN table entries) mixed in."""
+    import torch
+
+    import paper_2406_09904_b200 as Q
+
+    rng = np.random.default_rng(k + 1)
+    all16 = np.arange(0, 0x7C00, dtype=np.uint16).view(np.float16)
+    for m in (1, 16, 256, 300):
+        x16 = (rng.standard_normal((m, k)) * rng.uniform(0.1, 8.0, (m, 1))).astype(np.float16)
+        flat = x16.reshape(-1)
+        n = min(flat.size, all16.size)
+        flat[:n] = all16[rng.permutation(all16.size)[:n]] * np.where(rng.random(n) < 0.5, -1, 1).astype(np.float16)
+        s = np.ones(k)
+        sel = rng.choice(k, k // 8, replace=False)
+        s[sel] = rng.uniform(0.05, 20.0, k // 8)
+        s[sel[:4]] = [1e-130, 3e200, 2.0 ** -400, 2.0 ** 400]
+        want = O.quant_act_per_token(x16.astype(np.float64) / s)
+        st = torch.from_numpy(s).cuda()
+        recip = Q.smoothing_reciprocal(st)
+        r = recip.cpu().numpy()
+        ok = (np.abs(s) >= 2.0 ** -400) & (np.abs(s) <= 2.0 ** 400)
+        assert np.array_equal(r[ok].view(np.uint64), (1.0 / s[ok]).view(np.uint64)) and np.isnan(r[~ok]).all()
+        got = Q.quant_act_smoothed(torch.from_numpy(x16).cuda(), st, recip=recip)
+        assert np.array_equal(got.q.cpu().numpy(), want.q), (k, m)
+        assert np.array_equal(got.s_a.cpu().numpy().view(np.uint64), want.s_a.view(np.uint64)), (k, m)
+        assert np.array_equal(got._rowsum[1].cpu().numpy(), want.q.sum(1, dtype=np.int64)), (k, m)
