@@ -10,7 +10,8 @@ activations already quantized and resident in HBM; weights are read cold
 
 `value` = aggregate TOPS of the step (2*M*N*K summed / device time), max over
 ranks. `e2e` = the same sweep through the public API from pinned host fp16
-activations (H2D + quant_act_per_token + GEMM + D2H of y, every step).
+activations (H2D + quant_act_per_token + GEMM + D2H of y, every step; the copies
+run on their own streams, overlapped with the GEMMs).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -51,6 +52,22 @@ def alg_bytes(m, k, n, scheme="per-group", g=GROUP):
     """Algorithmic bytes per GEMM: int8 A + f64 s_A + int4 W + fp16 Y + scales."""
     sc = 8 * n if scheme == "per-channel" else 2 * (k // g) * n + 8 * n
     return m * k + 8 * m + k * n / 2 + 2 * m * n + sc
+
+
+TRAFFIC_FILE = "profiles/r01_traffic.json"
+
+
+def load_traffic(shapes, ms):
+    """DRAM bytes per step measured by ncu (scripts/traffic_summary.py), only when
+    the committed capture covers exactly this step's GEMMs."""
+    try:
+        with open(os.path.join(ROOT, TRAFFIC_FILE)) as f:
+            t = json.load(f)
+    except Exception:
+        return None
+    want = sorted("%dx%d/%d" % (k, n, m) for (k, n) in shapes for m in ms)
+    have = sorted("%s/%d" % (p["shape"], p["M"]) for p in t["points"])
+    return t if want == have else None
 
 
 # ---------------------------------------------------------------------------
@@ -333,7 +350,7 @@ def c4_stack_points(peaks, dev, batches=(1, 16, 64, 256)):
             sm = torch.ones(k, dtype=torch.float64, device=dev)
             idx = torch.randperm(k, device=dev)[: k // 8]
             sm[idx] = 0.5 + 1.5 * torch.rand(k // 8, dtype=torch.float64, device=dev)
-            lin.append((k, n, prep, sm))
+            lin.append((k, n, prep, sm, Q.smoothing_reciprocal(sm)))  # (the layer's cached table)
         layers.append(lin)
     r16 = max(2, math.ceil(2.5 * L2_BYTES / (4 * layer_bytes)))
     w16 = [[torch.randn((k, n), dtype=torch.float16, device=dev) for _, k, n in C4_LINEARS] for _ in range(r16)]
@@ -346,8 +363,8 @@ def c4_stack_points(peaks, dev, batches=(1, 16, 64, 256)):
 
         def stack_fn(lin):
             def f():
-                for i, (k, n, prep, sm) in enumerate(lin):
-                    aq = Q.quant_act_smoothed(xs[i], sm, check=False)
+                for i, (k, n, prep, sm, rc) in enumerate(lin):
+                    aq = Q.quant_act_smoothed(xs[i], sm, check=False, recip=rc)
                     G.run_gemm(aq, prep, n, False, y_out=ys[i])
             return f
 
@@ -477,33 +494,80 @@ def run_gpu_arm(args, world, rank, local):
         for si, (k, n) in enumerate(shapes):
             qws[(k, n)] = make_weights(k, n, scheme, seed=1000 + si + 17 * rank, device=dev)[:2]
 
+        # H2D, compute and D2H on three streams (PCIe is full duplex): input i+1
+        # uploads and output i-1 downloads while GEMM i runs; every byte still
+        # crosses the bus inside the timed region
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
         def e2e_step():
+            comp = torch.cuda.current_stream(dev)  # (the capture stream while a graph is captured)
+            s_in.wait_stream(comp)  # the previous step is done with dev_x
             for (k, n, m) in order:
                 dx = dev_x[(k, n, m)]
-                dx.copy_(host_x[(k, n, m)], non_blocking=True)
+                with torch.cuda.stream(s_in):
+                    dx.copy_(host_x[(k, n, m)], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(s_in)
+                comp.wait_event(ev)
                 aq = Q.quant_act_per_token(dx, check=False)
                 qw, fused = qws[(k, n)]
                 out = Q.w4a8_gemm_per_group(aq, qw, fused, with_acc=False)
-                host_y[(k, n, m)].copy_(out.y, non_blocking=True)
+                s_out.wait_stream(comp)
+                out.y.record_stream(s_out)
+                with torch.cuda.stream(s_out):
+                    host_y[(k, n, m)].copy_(out.y, non_blocking=True)
+            comp.wait_stream(s_out)
 
-        for _ in range(args.warmup):
+        def timed(step):
+            for _ in range(args.warmup):
+                step()
+            torch.cuda.synchronize()
+            barrier(world)
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                step()
+            torch.cuda.synchronize()
+            return max_over_ranks(time.perf_counter() - t0, world)
+
+        t_eager = timed(e2e_step)
+        # The same public-API calls captured once in a CUDA graph (as a serving
+        # loop would): each replay still uploads every input from pinned host
+        # memory and downloads every y; only the Python dispatch is gone.
+        t_graph, mode = None, "eager"
+        try:
             e2e_step()
-        barrier(world)
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_step()
-        torch.cuda.synchronize()
-        t_e2e = max_over_ranks(time.perf_counter() - t0, world)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                e2e_step()
+            # the replays really move the bytes: a fresh input pattern must come back as its y
+            key = order[-1]
+            host_x[key].copy_(torch.randn(host_x[key].shape, dtype=torch.float16))
+            g.replay()
+            torch.cuda.synchronize()
+            want = Q.w4a8_gemm_per_group(Q.quant_act_per_token(host_x[key].to(dev)), *qws[key[:2]], with_acc=False).y
+            if not torch.equal(host_y[key], want.cpu()):
+                raise RuntimeError("graph replay did not round-trip the host buffers")
+            t_graph, mode = timed(g.replay), "cuda graph of the API calls"
+        except Exception as exc:  # capture unsupported here: report the eager loop
+            mode = f"eager (graph capture failed: {type(exc).__name__}: {exc})"
+        t_e2e = t_graph if t_graph is not None else t_eager
         bi = sum(m * k * 2 for (k, n, m) in order)
         bo = sum(m * n * 2 for (k, n, m) in order)
-        e2e = dict(value=sum_over_ranks(ops_step * args.steps, world) / t_e2e / 1e12, unit="TOPS",
-                   h2d_bytes_per_step=bi, d2h_bytes_per_step=bo, ms_per_step=t_e2e / args.steps * 1e3)
+        tops = lambda t: sum_over_ranks(ops_step * args.steps, world) / t / 1e12
+        e2e = dict(value=tops(t_e2e), unit="TOPS", h2d_bytes_per_step=bi, d2h_bytes_per_step=bo,
+                   ms_per_step=t_e2e / args.steps * 1e3, mode=mode, eager_value=tops(t_eager),
+                   eager_ms_per_step=t_eager / args.steps * 1e3)
 
     # ---- roofline of the dominant kernel (the W4A8 GEMM: every launch in the step)
     step_us = ms_per_step * 1e3
     tops = ops_step / (step_us * 1e-6) / 1e12
+    traffic = load_traffic(shapes, ms)
     roofline = dict(bound="tensor", achieved=round(tops, 2), peak=round(int8_peak, 1), unit="TFLOP/s",
-                    frac=round(tops / int8_peak, 4), traffic=None,
+                    frac=round(tops / int8_peak, 4), traffic=traffic and traffic["step_dram_bytes"],
+                    traffic_note=traffic and ("bytes per step (the 33 GEMM launches) from ncu dram__bytes_read.sum "
+                                              "+ dram__bytes_write.sum, %s; %.3f x the algorithmic bytes" % (
+                                                  TRAFFIC_FILE, traffic["step_ratio"])),
                     peak_source=f"2 x bf16_tflops of MEASURED_PEAKS.json ({peaks['source']}); dense INT8 = 2x bf16",
                     roofline_frac_step=round(tot_roof_t / sum(p["us"] for p in points), 4),
                     note="achieved = sum(2MNK) over the step's 33 launches / device time; per-point bounds "
