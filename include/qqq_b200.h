@@ -201,6 +201,14 @@ int qqq_test_fast_f16_to_i8(const uint16_t* bits, int8_t* out, int64_t n, qqq_st
 int qqq_device_ok(void); /* QQQ_OK iff the current device is sm_100 */
 const char* qqq_version(void);
 
+/* ---- offline calibration ------------------------------------------
+ * matmul_ref (numerics.py:94-109) on the GPU: C = A B in f64 with the reference's
+ * rounding sequence (each product rounded, then added, in sequential k order;
+ * no FMA), so smoothing_objective's error matrix (smoothing.py:108-113) is
+ * bit-identical. A M x K, B K x N, C M x N, all row-major and contiguous. */
+int qqq_matmul_ref_f64(const double* a, const double* b, double* c, int64_t M, int64_t K, int64_t N,
+                       qqq_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif
