@@ -208,6 +208,15 @@ const char* qqq_version(void);
  * bit-identical. A M x K, B K x N, C M x N, all row-major and contiguous. */
 int qqq_matmul_ref_f64(const double* a, const double* b, double* c, int64_t M, int64_t K, int64_t N,
                        qqq_stream_t stream);
+/* One block [i1, i2) of the GPTQ column sweep (gptq.py:161-181) over work (f64
+ * K x N, row-major, updated in place), U = chol_inv (f64 K x K). gs = 0:
+ * per-channel with the frozen scales scale_row[N]; gs > 0: per-group, s_wg
+ * ((K/gs) x N) written at each group start (i1, i2 multiples of gs). Writes the
+ * codes (int8 K x N, rows i1..i2) and the block's errors eb ((i2-i1) x N).
+ * Bit-identical to the reference's block; the trailing update between blocks
+ * (gptq.py:182-183) is a BLAS product left to the caller. */
+int qqq_gptq_block(double* work, int64_t K, int64_t N, const double* u, int64_t i1, int64_t i2, int64_t gs,
+                   double* scale_row, double* s_wg, int8_t* codes, double* eb, qqq_stream_t stream);
 
 #ifdef __cplusplus
 }

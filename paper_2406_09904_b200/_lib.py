@@ -39,6 +39,7 @@ SIGNATURES = {
     "qqq_act_quant_smooth": (c_int, [P, c_int, I64, I64, I64, P, P, P, I64, P, P, P, S]),
     "qqq_smooth_reciprocal": (c_int, [P, I64, P, S]),
     "qqq_matmul_ref_f64": (c_int, [P, P, P, I64, I64, I64, S]),
+    "qqq_gptq_block": (c_int, [P, I64, I64, P, I64, I64, I64, P, P, P, P, S]),
     "qqq_act_quant_smooth_rcp": (c_int, [P, c_int, I64, I64, I64, P, P, P, I64, P, P, P, S]),
     "qqq_act_absmax": (c_int, [P, c_int, I64, I64, I64, P, P, S]),
     "qqq_act_quant_with_max": (c_int, [P, c_int, I64, I64, I64, P, P, I64, P, P, P, S]),
