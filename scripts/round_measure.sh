@@ -17,6 +17,10 @@ if [ -z "$NONCU" ]; then
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
       python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --quick > gpurun_out/ncu_bench.log 2>&1
   echo "ncu launch list exit $?" >> gpurun_out/ncu_bench.log
+  # DRAM bytes of every GEMM of the bench step (-> scripts/traffic_summary.py -> profiles/rNN_traffic.json)
+  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+      -k regex:w4a8_gemm --csv --log-file gpurun_out/traffic.csv \
+      python scripts/quick_bench.py --profile --ms 1,2,4,8,16,32,64,128,256,512,1024 > gpurun_out/traffic.log 2>&1
   # full captures of the dominant kernel at decode / mid / prefill M
   for spec in "4096x11008 1024" "4096x11008 128" "4096x11008 16" "4096x11008 1"; do
     set -- $spec
