@@ -99,7 +99,8 @@ def quant_act_smoothed(x, s, check: bool = True, recip: torch.Tensor = None) -> 
         if recip is not None:
             if tuple(recip.shape) != (k,) or recip.dtype != torch.float64 or recip.device != dev:
                 raise ShapeError("recip must be smoothing_reciprocal(s) on the activations' device")
-            rc = lib.qqq_act_quant_smooth_rcp(_lib.ptr(xt), dt, m, k, ldx, _lib.ptr(st), _lib.ptr(recip.contiguous()),
+            recip = recip.contiguous()
+            rc = lib.qqq_act_quant_smooth_rcp(_lib.ptr(xt), dt, m, k, ldx, _lib.ptr(st), _lib.ptr(recip),
                                               _lib.ptr(qbuf), kp, _lib.ptr(s_a), _lib.ptr(rowsum), _lib.ptr(status),
                                               _lib.stream_of(dev))
         else:

@@ -77,3 +77,50 @@ def test_gpu_build_hessian_and_sweep_close_to_reference():
         Q.build_hessian(np.zeros((3, 4)))
     with pytest.raises(Q.ShapeError):
         Q.gptq_sweep(np.zeros((8, 4)), Q.build_hessian(np.ones((3, 16))), Q.QuantSpec("per-channel"))
+
+
+def _single_block_sweep(w, u, g):
+    """gptq.py:155-181 for one block covering all of K (test-side restatement,
+    vectorised over the output columns)."""
+    k, n = w.shape
+    wb = w.copy()
+    codes = np.empty((k, n), dtype=np.int8)
+    scales = np.empty((k // g, n)) if g else None
+    scale_row = None
+    if not g:
+        mx = np.abs(wb).max(axis=0)
+        scale_row = np.where(mx > 0.0, mx / 7.0, 1.0)
+        scales = scale_row
+    for i in range(k):
+        if g and i % g == 0:
+            gm = np.abs(wb[i:i + g, :]).max(axis=0)
+            scale_row = np.where(gm > 0.0, gm / 7.0, 1.0)
+            scales[i // g] = scale_row
+        row = wb[i, :]
+        q = np.clip(np.rint(row / scale_row), -8, 7)
+        codes[i] = q.astype(np.int8)
+        err = (row - q * scale_row) / u[i, i]
+        wb[i + 1:, :] -= np.outer(u[i, i + 1:], err)
+    return codes, scales
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g", [0, 128])
+def test_gpu_gptq_large_single_block(g):
+    """A 1024-row block (beyond the shared-memory staging, updated in place in
+    global memory) bit-identical to the single-block sweep."""
+    import paper_2406_09904_b200 as Q
+
+    rng = np.random.default_rng(17 + g)
+    k, n = 1024, 40
+    w = rng.standard_normal((k, n)) * 0.05
+    u = np.triu(rng.standard_normal((k, k)) * 0.01)
+    u[np.diag_indices(k)] = rng.uniform(0.5, 2.0, k)
+    hs = Q.HessianState(hessian=np.zeros((k, k)), damping=0.0, chol_inv=u, dead=np.zeros(k, bool),
+                        samples=rng.standard_normal((4, k)))
+    spec = Q.QuantSpec("per-group", g) if g else Q.QuantSpec("per-channel")
+    res = Q.gptq_sweep(w, hs, spec, block_size=k)
+    codes, scales = _single_block_sweep(w, u, g)
+    assert np.array_equal(res.qweights.codes().cpu().numpy(), codes)
+    got = (res.qweights.s_wg if g else res.qweights.s_w).cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), scales.view(np.uint64))
