@@ -440,3 +440,36 @@ def test_c2_golden_digests(digests):
         assert O.digest(np_(aq.q)) == d["q"]
         assert O.digest(np_(qw.packed)) == d["packed"] and O.digest(np_(fused.s_star)) == d["s_star"]
         assert O.digest(np_(out.acc)) == d["acc"] and O.digest(np_(out.y)) == d["y"]
+
+
+@pytest.mark.parametrize("m,n,ntok,split", [(64, 256, 0, -1), (1024, 512, 0, -1), (200, 384, 128, 1),
+                                            (16, 512, 16, 4)])
+def test_gemm_epilogue_exact_f16_ties(m, n, ntok, split):
+    """Outputs on exact f16 rounding midpoints: integer activations with s_a = 1
+    and weights q * 2^-8 (s_w = 2^-8) make y = a * 2^-8 (a = sum x q), a tie
+    whenever a is odd in [2048, 4096) (or 2 mod 4 in [4096, 8192), ...). The epilogue's fp32
+    fast path must hand every tie (and every value near one) to the f64 path:
+    y bit-identical to the reference's f16((acc * s_a) * s_w/16), ties to even."""
+    rng = np.random.default_rng(m + n)
+    k = 256
+    x = rng.integers(-127, 128, (m, k)).astype(np.float64)
+    x[:, 0] = 127.0  # s_a = 127 / 127 = 1
+    q = rng.integers(-7, 8, (k, n))
+    q[0, :] = 7  # column max 7 * 2^-8 -> s_w = 2^-8, codes = q
+    w = q * 2.0 ** -8
+    qw_o = O.quant_weight_per_channel(w)
+    assert np.all(qw_o.s_w == 2.0 ** -8)
+    x16 = x.astype(np.float16)
+    aq_o = O.quant_act_per_token(x16.astype(np.float64))
+    want = O.w4a8_gemm_per_channel(aq_o, qw_o, O.FusedScales.from_quantized(qw_o), fast=True)
+    a = want.acc.astype(np.int64) // 16  # acc carries the x16 of w8 = 16 q (gemm.py:180)
+    assert np.sum((np.abs(a) >= 2048) & (np.abs(a) < 4096) & (a % 2 == 1)) > 0  # ties present
+    qw = _to_gpu_qw(qw_o)
+    fused = Q.FusedScales.from_quantized(qw)
+    aq = Q.quant_act_per_token(torch.from_numpy(x16).cuda())
+    from paper_2406_09904_b200 import gemm as G
+
+    cfg = None if ntok == 0 else {"ntok": ntok, "split": split}
+    out = G.run_gemm(aq, G.prepare(qw, fused), n, True, cfg=cfg)
+    assert same_bits(out.acc, want.acc)
+    assert same_bits(out.y, want.y), (m, n, ntok, split)
