@@ -138,3 +138,28 @@ def test_faithful_and_fast_gemm_agree():
     a = rng.integers(-127, 128, (8, 2048)).astype(np.int8)
     b = rng.integers(-128, 128, (2048, 24)).astype(np.int8)
     assert np.array_equal(O.gemm_i8_i32(a, b), O.gemm_i8_i32_fast(a, b))
+
+
+def test_oracle_calibration_vs_reference_goldens():
+    """The calibration restatements reproduce the reference's own outputs
+    (tests/golden/make_golden_{smoothing,gptq}.py): search_sigma's plan and
+    candidate objectives exactly, the GPTQ sweep's codes and scales exactly."""
+    import os
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    d = np.load(os.path.join(here, "smoothing_cases.npz"))
+    for i in range(int(d["n_cases"])):
+        m, k, n, g = (int(v) for v in d[f"c{i}_meta"])
+        x, w = d[f"c{i}_x"], d[f"c{i}_w"]
+        assert np.array_equal(O.matmul_ref(x, w).view(np.uint64), d[f"c{i}_exact"].view(np.uint64))
+        sigma, sel, s, obj = O.search_sigma(x, w, g if bool(d[f"c{i}_pg"]) else 0, int(d[f"c{i}_grid"]))
+        assert sigma == float(d[f"c{i}_sigma"]) and obj == float(d[f"c{i}_obj"])
+        assert sel == tuple(int(t) for t in np.flatnonzero(d[f"c{i}_sel"]))
+        assert np.array_equal(s.view(np.uint64), d[f"c{i}_s"].view(np.uint64))
+    d = np.load(os.path.join(here, "gptq_cases.npz"))
+    for i in range(int(d["n_cases"])):
+        m, k, n, g, bs = (int(v) for v in d[f"c{i}_meta"])
+        codes, scales, col_err = O.gptq_sweep(d[f"c{i}_w"], d[f"c{i}_u"], d[f"c{i}_dead"], g, bs)
+        assert np.array_equal(codes, d[f"c{i}_codes"]), i
+        assert np.array_equal(scales.view(np.uint64), d[f"c{i}_scales"].view(np.uint64)), i
+        assert np.array_equal(col_err.view(np.uint64), d[f"c{i}_col_errors"].view(np.uint64)), i

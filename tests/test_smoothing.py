@@ -91,3 +91,26 @@ def test_gpu_search_sigma_matches_reference_plan():
         Q.search_sigma(np.ones((2, 4)), np.ones((4, 2)), Q.QuantSpec("per-channel"), grid_points=1)
     z = Q.search_sigma(np.zeros((2, 4)), np.ones((4, 2)), Q.QuantSpec("per-channel"), grid_points=4)
     assert z.selected == () and z.sigma == 1.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g", [0, 64])
+def test_gpu_search_sigma_random_vs_oracle(g):
+    """Seeded random calibration sets (outlier channels, a zero channel) against
+    the oracle restatement (oracle/qqq_oracle.py search_sigma, pinned to the
+    reference goldens): same plan, objective within 1e-12."""
+    import paper_2406_09904_b200 as Q
+    from oracle import qqq_oracle as O
+
+    rng = np.random.default_rng(100 + g)
+    for (m, k, n) in [(8, 128, 32), (20, 192, 24)]:
+        x = rng.standard_normal((m, k))
+        x[:, rng.choice(k, 6, replace=False)] *= rng.uniform(8.0, 60.0, 6)
+        x[:, 3] = 0.0
+        w = rng.standard_normal((k, n)) * 0.1
+        sigma, sel, s, obj = O.search_sigma(x, w, g, grid_points=10)
+        spec = Q.QuantSpec("per-group", g) if g else Q.QuantSpec("per-channel")
+        plan = Q.search_sigma(x, w, spec, grid_points=10)
+        assert plan.sigma == sigma and plan.selected == sel, (m, k, n)
+        assert np.array_equal(np.asarray(plan.s).view(np.uint64), s.view(np.uint64))
+        assert abs(plan.objective - obj) <= 1e-12 * obj
