@@ -158,3 +158,31 @@ def test_gpu_gptq_random_vs_oracle(g, bs):
         assert np.mean(got_codes == codes) >= 0.999
         np.testing.assert_allclose(got_scales, scales, rtol=1e-9)
     np.testing.assert_allclose(res.col_errors.cpu().numpy(), col_err, rtol=1e-9)
+
+
+@pytest.mark.gpu
+def test_gpu_calibration_to_serving_example():
+    """INTEGRATION.md's calibration example runs end to end (smoothing search ->
+    Hessian -> GPTQ -> apply_quant_linear) and agrees with the oracle's
+    apply_quant_linear on the resulting layer."""
+    import torch
+
+    import paper_2406_09904_b200 as qqq
+    from oracle import qqq_oracle as O
+
+    rng = np.random.default_rng(3)
+    x_calib = rng.standard_normal((32, 256))
+    x_calib[:, [5, 77]] *= 30.0
+    w = rng.standard_normal((256, 128)) * 0.05
+    spec = qqq.QuantSpec("per-group", 128)
+    plan = qqq.search_sigma(x_calib, w, spec)
+    hs = qqq.build_hessian(x_calib / plan.s)
+    res = qqq.gptq_sweep(w * plan.s[:, None], hs, spec)
+    layer = qqq.QuantizedLayer("fc1", res.qweights, plan)
+    x = torch.from_numpy(rng.standard_normal((8, 256))).cuda()
+    y = qqq.apply_quant_linear(x, layer).cpu().numpy()
+    qw = res.qweights
+    qw_o = O.QuantizedWeights(qw.packed.cpu().numpy(), qw.rows, qw.cols, O.PER_GROUP, 128,
+                              s_wg=qw.s_wg.cpu().numpy(), s_wc=qw.s_wc.cpu().numpy())
+    want = O.apply_quant_linear(x.cpu().numpy(), plan.s, qw_o)
+    assert np.array_equal(y.view(np.uint64), want.view(np.uint64))
