@@ -172,6 +172,7 @@ typedef struct qqq_gemm_config {
               * 3 whole 256x256 pair tiles (2-CTA clusters, ntok 256), 4 cluster split-K
               * (ntok 16/32: one tile per cluster, DSMEM reduction), 5 stream-K over pair
               * tiles, 6 pair-tile waves + stream-K remainder */
+  int csplit; /* split 4 only: cluster size S in 2..8 (0 = the planner's choice) */
   void* dbg; /* optional device buffer [grid][64] u64: per-CTA %globaltimer timeline (diagnostics) */
 } qqq_gemm_config;
 
@@ -179,6 +180,13 @@ int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a,
                      const void* w_repacked, int64_t group, const double* s_col, int64_t M, int64_t N, int64_t K,
                      void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
                      const qqq_gemm_config* cfg, qqq_stream_t stream);
+
+/* The tile plan qqq_w4a8_gemm_ex would launch for (mode, M, N, K, cfg): the
+ * planner's choice when cfg is NULL or all-auto, else the forced plan as the
+ * launch resolves it (out->split is the effective split, out->csplit the
+ * cluster size of split 4). Diagnostics and tests; no device work. */
+int qqq_gemm_plan_info(int mode, int64_t M, int64_t N, int64_t K, const qqq_gemm_config* cfg,
+                       qqq_gemm_config* out);
 
 /* The dequant epilogue alone (gemm.py:182-184 / 200-202): y f16 M x N =
  * f16((acc*s_a)*s_col) in f64; used after an exact int32 all-reduce of K-split
@@ -198,6 +206,11 @@ int qqq_test_pc_convert(const int8_t* q, int8_t* out, int64_t n, qqq_stream_t st
 int qqq_test_fast_f16_to_i8(const uint16_t* bits, int8_t* out, int64_t n, qqq_stream_t stream);
 
 /* ---- misc ---------------------------------------------------------------- */
+/* Dense INT8 tensor-core peak probe (bench.py's roofline denominator): `grid`
+ * CTAs (one per SM) each issue `iters` (multiple of 8) back-to-back
+ * tcgen05.mma kind::i8 M=128 N=256 K=32 from shared memory; *ops_out = the
+ * integer ops the launch performs. The caller times it with CUDA events. */
+int qqq_probe_int8_peak(int grid, int iters, double* ops_out, qqq_stream_t stream);
 int qqq_device_ok(void); /* QQQ_OK iff the current device is sm_100 */
 const char* qqq_version(void);
 

@@ -24,7 +24,7 @@ MODE_PC, MODE_PG, MODE_I8 = 0, 1, 2
 
 
 class GemmConfig(ctypes.Structure):
-    _fields_ = [("ntok", c_int), ("grid", c_int), ("split", c_int), ("dbg", c_void_p)]
+    _fields_ = [("ntok", c_int), ("grid", c_int), ("split", c_int), ("csplit", c_int), ("dbg", c_void_p)]
 
 
 P = c_void_p
@@ -58,9 +58,11 @@ SIGNATURES = {
     "qqq_w4a8_gemm_pg": (c_int, [P, I64, P, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t, S]),
     "qqq_w4a8_gemm_ex": (c_int, [c_int, P, I64, P, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t,
                                   ctypes.POINTER(GemmConfig), S]),
+    "qqq_gemm_plan_info": (c_int, [c_int, I64, I64, I64, ctypes.POINTER(GemmConfig), ctypes.POINTER(GemmConfig)]),
     "qqq_test_fused_dequant_quant": (c_int, [P, P, P, I64, c_int, S]),
     "qqq_test_pc_convert": (c_int, [P, P, I64, S]),
     "qqq_test_fast_f16_to_i8": (c_int, [P, P, I64, S]),
+    "qqq_probe_int8_peak": (c_int, [c_int, c_int, P, S]),
     "qqq_device_ok": (c_int, []),
     "qqq_version": (c_char_p, []),
 }
@@ -90,19 +92,43 @@ def load() -> ctypes.CDLL:
     return _lib
 
 
-def lib_for_device(device) -> ctypes.CDLL:
-    """The library, after checking that `device` is an sm_100 GPU."""
+class _OnDevice:
+    """The library with every entry point called under `torch.cuda.device(idx)`:
+    the C ABI launches on the calling thread's current device, so a call for a
+    tensor on another GPU of the process switches to it for the call."""
+
+    def __init__(self, lib, idx: int):
+        self._lib = lib
+        self._idx = idx
+
+    def __getattr__(self, name):
+        import torch
+
+        fn = getattr(self._lib, name)
+        idx = self._idx
+
+        def call(*args):
+            with torch.cuda.device(idx):
+                return fn(*args)
+
+        return call
+
+
+def lib_for_device(device):
+    """The library, after checking that `device` is an sm_100 GPU. When `device`
+    is not the current device, the returned handle switches to it per call."""
     import torch
 
     lib = load()
     idx = torch.device(device).index
-    idx = torch.cuda.current_device() if idx is None else idx
+    cur = torch.cuda.current_device()
+    idx = cur if idx is None else idx
     if idx not in _device_checked:
         major, minor = torch.cuda.get_device_capability(idx)
         if (major, minor) != (10, 0):
             raise KernelError(f"device {idx} is sm_{major}{minor}; the kernels are built for sm_100a only")
         _device_checked.add(idx)
-    return lib
+    return lib if idx == cur else _OnDevice(lib, idx)
 
 
 _RC = {

@@ -205,7 +205,7 @@ def _layer_from(meta: dict, name: str, get, device, prepare: bool):
     """pipeline.py:254-281 on the GPU: the scale tensors are the stored f32
     values widened to f64, as the reference's `.astype(np.float64)`."""
     from . import gemm as G
-    from .pipeline import QuantizedLayer, SmoothingPlan
+    from .pipeline import QuantizedLayer, SmoothingPlan, layer_fused_scales
     from .quantize import PER_CHANNEL, PER_GROUP, QuantizedWeights
 
     if name not in meta:
@@ -226,9 +226,7 @@ def _layer_from(meta: dict, name: str, get, device, prepare: bool):
                          s=np.asarray(sm["s"], dtype=np.float64), objective=float(sm["objective"]))
     layer = QuantizedLayer(name=name, qweights=qw, plan=plan)
     if prepare:  # the GPU repack into the tile layout now, not at the first GEMM
-        fused = G.FusedScales.from_quantized(qw)
-        layer._cache["fused"] = fused
-        G.prepare(qw, fused)
+        G.prepare(qw, layer_fused_scales(layer))
     return layer
 
 

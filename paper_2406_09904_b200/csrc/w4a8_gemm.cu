@@ -1049,9 +1049,23 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           if (lead) {
             int32_t* cnt = p.counters + slot_id;
             int v;
-            do {
+            unsigned long long t0 = 0;
+#pragma unroll 1
+            for (uint32_t n = 0;; ++n) {
               asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-            } while (v < nsegs - 1);
+              if (v >= nsegs - 1) break;
+#ifndef QQQ_NO_WATCHDOG
+              // a contributor that never arrives (not co-resident, corrupted
+              // counters) traps the launch after ~4 s instead of hanging the GPU
+              if ((n & 1023) == 1023) {
+                const unsigned long long t = gtimer();
+                if (t0 == 0)
+                  t0 = t;
+                else if (t - t0 > 4000000000ull)
+                  __trap();
+              }
+#endif
+            }
             *cnt = 0;  // re-arm for the next launch (every contributor has arrived)
             QQQ_STAMP(60);
           }
@@ -1167,15 +1181,29 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-static int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+// Per-device host caches (SM counts, co-resident pair clusters, kernel
+// attributes): the C ABI runs on the calling thread's current device, which
+// the caller sets to the stream's device (the Python layer does).
+constexpr int kMaxDevices = 64;
+
+static int cur_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    cudaGetLastError();
+    dev = 0;
   }
-  return n;
+  return dev;
+}
+
+static int num_sms() {
+  static int n[kMaxDevices] = {};
+  const int dev = cur_device();
+  if (n[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
+  }
+  return n[dev];
 }
 
 struct LaunchPlan {
@@ -1203,7 +1231,8 @@ __global__ void w4a8_gemm_kernel(const __grid_constant__ CUtensorMap, const __gr
 // 2-CTA clusters of the pair kernel that fit on the GPU at once (a GPC with an
 // odd number of free SMs strands one): the stream-K pair plans never exceed it
 static int pair_slots(int mode) {
-  static int n[2] = {0, 0};
+  static int slots[kMaxDevices][2] = {};
+  int* n = slots[cur_device()];
   const int i = mode == kModePC ? 0 : 1;
   if (n[i] == 0) {
     using C = Cfg<kModePG, 256, kPairBk, true>;
@@ -1234,7 +1263,8 @@ static int pair_slots(int mode) {
 // split: 0 = whole tiles (data-parallel), 1 = stream-K over all units,
 //        2 = hybrid: full waves of whole tiles, the remainder stream-K'd over all CTAs,
 //        3 = whole 256-channel pair tiles on 2-CTA clusters (NTOK = 256, PC/PG)
-static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, int split, int force_grid) {
+static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, int split, int force_grid,
+                           int force_cs = 0) {
   LaunchPlan lp{};
   // cluster split-K: decode tiles only (NTOK 16/32, 2 CTAs per SM). (A 128-token
   // prefill variant — 64 KiB partials over DSMEM — measured slower than stream-K:
@@ -1263,10 +1293,14 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
       return (int64_t)lp.tiles * c <= slots && c <= lp.kb_per_tile && c * rows_per * ntok * 4 <= 16384;
     };
     int S = 1;
-    for (int c = 2; c <= 8; ++c) {
-      if (!fits(c)) continue;
-      S = c;  // the largest fitting S, unless a smaller one meets both targets below
-      if (lp.tiles * c * 5 >= num_sms() * 4 && (lp.kb_per_tile + c - 1) / c <= 8) break;
+    if (force_cs >= 2 && force_cs <= 8 && fits(force_cs)) {
+      S = force_cs;  // caller's cluster size (tests of every S the rule below can pick)
+    } else {
+      for (int c = 2; c <= 8; ++c) {
+        if (!fits(c)) continue;
+        S = c;  // the largest fitting S, unless a smaller one meets both targets below
+        if (lp.tiles * c * 5 >= num_sms() * 4 && (lp.kb_per_tile + c - 1) / c <= 8) break;
+      }
     }
     if (S == 1) return plan_for(mode, M, N, K, ntok, 1, force_grid);
     lp.csplit = S;
@@ -1395,11 +1429,11 @@ static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
 }
 
 static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force_ntok, int force_grid,
-                            int force_split) {
+                            int force_split, int force_cs = 0) {
   if (force_ntok > 0 || force_split >= 0 || force_grid > 0) {
     const int nt = force_ntok > 0 ? force_ntok : (M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256);
     const int sk = force_split >= 0 ? force_split : (nt <= 64 ? 1 : 2);
-    return plan_for(mode, M, N, K, nt, sk, force_grid);
+    return plan_for(mode, M, N, K, nt, sk, force_grid, force_cs);
   }
   LaunchPlan best{};
   double best_t = 1e30;
@@ -1440,11 +1474,12 @@ static int launch_t(const CUtensorMap& map, const CUtensorMap& ymap, const GemmP
                     cudaStream_t stream) {
   using C = Cfg<MODE, NTOK, BK, PAIR>;
   auto kern = w4a8_gemm_kernel<MODE, NTOK, BK, PAIR>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};  // per instantiation and device
+  const int dev = cur_device();
+  if (!attr_set[dev]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
       return kErrCuda;
-    attr_set = true;
+    attr_set[dev] = true;
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(grid);
@@ -1505,6 +1540,26 @@ extern "C" size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   return best;
 }
 
+// The tile plan a launch with these arguments would use (the planner's pick,
+// or the forced plan resolved the way the launch resolves it).
+extern "C" int qqq_gemm_plan_info(int mode, int64_t M, int64_t N, int64_t K, const qqq_gemm_config* cfg,
+                                  qqq_gemm_config* out) {
+  if (M <= 0 || N <= 0 || K <= 0 || !out) return kErrShape;
+  const LaunchPlan lp = make_plan(mode, M, N, K, cfg ? cfg->ntok : 0, cfg ? cfg->grid : 0, cfg ? cfg->split : -1,
+                                  cfg ? cfg->csplit : 0);
+  out->ntok = lp.ntok;
+  out->grid = lp.grid;
+  out->csplit = lp.csplit;
+  out->dbg = nullptr;
+  if (lp.csplit > 1)
+    out->split = 4;
+  else if (lp.pair)
+    out->split = lp.aligned_tiles > 0 ? 3 : lp.dp_tiles > 0 ? 6 : 5;
+  else
+    out->split = lp.aligned_tiles > 0 ? 0 : lp.dp_tiles > 0 ? 2 : 1;
+  return kOk;
+}
+
 // Generic entry: mode 0 = per-channel (PC), 1 = per-group (PG), 2 = pre-converted int8 (I8).
 extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const int32_t* rowsum,
                                 const void* w_repacked, int64_t group, const double* s_col, int64_t M, int64_t N,
@@ -1523,7 +1578,8 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return kErrCuda;
 
-  LaunchPlan lp = make_plan(mode, M, N, K, cfg ? cfg->ntok : 0, cfg ? cfg->grid : 0, cfg ? cfg->split : -1);
+  LaunchPlan lp = make_plan(mode, M, N, K, cfg ? cfg->ntok : 0, cfg ? cfg->grid : 0, cfg ? cfg->split : -1,
+                            cfg ? cfg->csplit : 0);
   if (lp.tiles * (lp.pair ? 2 : 1) > kMaxTiles) return kErrUnsupported;
   if (ws_bytes < plan_ws_bytes(lp)) return kErrConfig;
 

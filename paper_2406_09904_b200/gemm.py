@@ -90,25 +90,44 @@ class GemmOutput:  # gemm.py:72-78
 
 _ws_lock = threading.Lock()
 _workspaces: dict = {}
+_retired: list = []  # outgrown workspaces stay allocated: captured CUDA graphs may still address them
 
 
-def workspace(device: torch.device, nbytes: int) -> torch.Tensor:
-    """Zeroed split-K workspace per device; every launch leaves it zeroed again.
+def workspace(device: torch.device, nbytes: int, stream=None) -> torch.Tensor:
+    """Zeroed split-K workspace (tile counters + partial slots) per (device,
+    stream); every launch leaves it zeroed again.
 
-    GEMMs that may run concurrently on different streams must pass their own
-    workspace (run_gemm(..., ws=...)); launches on one stream share this one.
+    GEMMs on one stream run in order, so they share one workspace; GEMMs on
+    different streams (which may overlap) get different ones. A workspace that
+    is outgrown is replaced but never freed, because a CUDA graph captured
+    earlier may still launch into it.
     """
-    key = device.index
+    dev = torch.device(device)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    st = torch.cuda.current_stream(dev) if stream is None else stream
+    key = (dev.index, st.cuda_stream)
     with _ws_lock:
         ws = _workspaces.get(key)
         if ws is None or ws.numel() < nbytes:
-            ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-            _workspaces[key] = ws
+            with torch.cuda.stream(st):
+                new = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+            if ws is not None:
+                _retired.append(ws)
+            ws = _workspaces[key] = new
     return ws
 
 
-def _version_key(t: torch.Tensor):
-    return (t.data_ptr(), t._version, tuple(t.shape))
+def _version_key(t):
+    """Cache key of a weight/scale operand: identity + in-place version for torch
+    tensors; identity + data pointer + a CRC of the bytes for host arrays (numpy
+    has no version counter, so in-place edits are caught by the checksum)."""
+    if isinstance(t, torch.Tensor):
+        return ("t", t.data_ptr(), t._version, tuple(t.shape), t.dtype)
+    import zlib
+
+    a = np.ascontiguousarray(np.asarray(t))
+    return ("np", id(t), a.__array_interface__["data"][0], a.shape, a.dtype.str, zlib.crc32(a.view(np.uint8).ravel()))
 
 
 def _pg_fast_ok(g: int) -> bool:
@@ -138,19 +157,20 @@ class PreparedWeights:
 def prepare(qw: QuantizedWeights, fused: FusedScales) -> PreparedWeights:
     """One-time repack (cached) of the reference packing into the tcgen05 blob.
 
-    Cache key: the identity and in-place version of qw.packed (and fused.s_star),
-    so a mutated or replaced tensor is repacked again.
+    Cache key: the identity and in-place version of qw.packed (and fused.s_star,
+    fused.s_wc), so a mutated or replaced operand is repacked again; host
+    (numpy) operands are keyed by identity and a checksum of their bytes.
     """
-    packed = as_cuda(qw.packed, torch.uint8).contiguous()
-    dev = packed.device
-    lib = _lib.lib_for_device(dev)
     k, n = qw.rows, qw.cols
-    if packed.shape != ((k + 1) // 2, n):
-        raise CorruptionError(f"packed shape {tuple(packed.shape)} inconsistent with K={k}, N={n}")
+    if tuple(qw.packed.shape) != ((k + 1) // 2, n):
+        raise CorruptionError(f"packed shape {tuple(qw.packed.shape)} inconsistent with K={k}, N={n}")
     if qw.scheme == PER_CHANNEL:
         key = ("pc", _version_key(qw.packed))
         hit = qw._cache.get("pc")
         if hit is None or hit[0] != key:
+            packed = as_cuda(qw.packed, torch.uint8).contiguous()
+            dev = packed.device
+            lib = _lib.lib_for_device(dev)
             w = torch.empty(lib.qqq_repacked_weight_bytes(_lib.MODE_PC, k, n, 0), dtype=torch.uint8, device=dev)
             _lib.check(lib.qqq_repack_weights(_lib.ptr(packed), None, k, n, _lib.MODE_PC, 0, _lib.ptr(w), None,
                                               _lib.stream_of(dev)), "repack_weights")
@@ -158,11 +178,14 @@ def prepare(qw: QuantizedWeights, fused: FusedScales) -> PreparedWeights:
             qw._cache["pc"] = hit
         return PreparedWeights(_lib.MODE_PC, hit[1], None, 0, as_cuda(fused.s_w_folded, torch.float64).contiguous())
     g = qw.group_size
-    s_star = as_cuda(fused.s_star, torch.float16).contiguous()
-    key = ("pg", _version_key(qw.packed), _version_key(fused.s_star), g)
+    key = ("pg", _version_key(qw.packed), _version_key(fused.s_star), _version_key(fused.s_wc), g)
     hit = fused._cache.get("pg")
     if hit is not None and hit[0] == key:
         return hit[1]
+    packed = as_cuda(qw.packed, torch.uint8).contiguous()
+    dev = packed.device
+    lib = _lib.lib_for_device(dev)
+    s_star = as_cuda(fused.s_star, torch.float16).contiguous()
     s_wc = as_cuda(fused.s_wc, torch.float64).contiguous()
     prep = None
     if _pg_fast_ok(g):
@@ -220,7 +243,7 @@ def run_gemm(aq: QuantizedActivations, prep: PreparedWeights, n: int, with_acc: 
     if cfg:
         dbg = cfg.get("dbg")
         c = _lib.GemmConfig(int(cfg.get("ntok", 0)), int(cfg.get("grid", 0)), int(cfg.get("split", -1)),
-                            None if dbg is None else dbg.data_ptr())
+                            int(cfg.get("csplit", 0)), None if dbg is None else dbg.data_ptr())
     ldq = q.stride(0) if m > 1 else (k + 127) // 128 * 128
     rs = rowsum_of(aq) if prep.mode == _lib.MODE_PG else None
     rc = lib.qqq_w4a8_gemm_ex(prep.mode, _lib.ptr(q), ldq, _lib.ptr(s_a), _lib.ptr(rs), _lib.ptr(prep.w),
@@ -229,6 +252,19 @@ def run_gemm(aq: QuantizedActivations, prep: PreparedWeights, n: int, with_acc: 
                               None if c is None else c, _lib.stream_of(dev))
     _lib.check(rc, "w4a8_gemm")
     return GemmOutput(y=y, acc=acc)
+
+
+def plan_info(mode: int, m: int, n: int, k: int, cfg: Optional[dict] = None) -> dict:
+    """The tile plan a GEMM launch would use (no device work): ntok, split,
+    grid, csplit. Split codes as in qqq_gemm_config (include/qqq_b200.h)."""
+    lib = _lib.load()
+    c = None
+    if cfg:
+        c = _lib.GemmConfig(int(cfg.get("ntok", 0)), int(cfg.get("grid", 0)), int(cfg.get("split", -1)),
+                            int(cfg.get("csplit", 0)), None)
+    out = _lib.GemmConfig()
+    _lib.check(lib.qqq_gemm_plan_info(mode, m, n, k, c, out), "gemm_plan_info")
+    return {"ntok": out.ntok, "split": out.split, "grid": out.grid, "csplit": out.csplit}
 
 
 def _check_gemm_operands(aq: QuantizedActivations, qw: QuantizedWeights, fused: FusedScales, scheme: str) -> None:

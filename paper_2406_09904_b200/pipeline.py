@@ -21,7 +21,7 @@ import torch
 
 from . import _lib
 from .errors import ShapeError
-from .gemm import FusedScales, w4a8_gemm_per_channel, w4a8_gemm_per_group
+from .gemm import FusedScales, _version_key, w4a8_gemm_per_channel, w4a8_gemm_per_group
 from .quantize import (PER_CHANNEL, QuantizedActivations, QuantizedWeights, as_cuda, attach_rowsum, deferred_status,
                        raise_if_bad)
 
@@ -116,16 +116,32 @@ def quant_act_smoothed(x, s, check: bool = True, recip: torch.Tensor = None) -> 
     return out
 
 
+def layer_fused_scales(layer: QuantizedLayer) -> FusedScales:
+    """FusedScales of the layer's weights, cached on the layer and keyed on the
+    identity and version of qweights and its scales (the reference rebuilds
+    them per call: they are a pure function of the weights, gemm.py:61-69)."""
+    qw = layer.qweights
+    fkey = (id(qw), qw.scheme, qw.group_size, qw.rows, qw.cols,
+            *(None if a is None else _version_key(a) for a in (qw.s_w, qw.s_wg, qw.s_wc)))
+    hit = layer._cache.get("fused")
+    if hit is None or hit[0] != fkey:
+        hit = layer._cache["fused"] = (fkey, FusedScales.from_quantized(qw))
+    return hit[1]
+
+
 def apply_quant_linear(x, layer: QuantizedLayer, check: bool = True) -> torch.Tensor:
     """Quantized forward of one linear (pipeline.py:144-152): divide by s,
     quantize, W4A8 GEMM; returns y widened to f64 (GemmOutput.y_wide)."""
-    recip = layer._cache.get("recip")
-    if recip is None:  # the plan's reciprocal table, once per layer
-        recip = layer._cache["recip"] = smoothing_reciprocal(layer.plan.s)
-    qa = quant_act_smoothed(x, layer.plan.s, check=check, recip=recip)
-    fused = layer._cache.get("fused")
-    if fused is None:  # the reference rebuilds FusedScales per call; it is a pure function of the weights
-        fused = FusedScales.from_quantized(layer.qweights)
-        layer._cache["fused"] = fused
-    run = w4a8_gemm_per_channel if layer.qweights.scheme == PER_CHANNEL else w4a8_gemm_per_group
-    return run(qa, layer.qweights, fused, with_acc=False).y_wide()
+    # Per-layer caches, keyed on the identity and version of what they were
+    # built from: a reassigned plan / qweights (or an in-place edit of s or of
+    # the weight scales) rebuilds them instead of reusing stale values.
+    s = layer.plan.s
+    rkey = (id(layer.plan), _version_key(s))
+    hit = layer._cache.get("recip")
+    if hit is None or hit[0] != rkey:  # the plan's reciprocal table, once per plan
+        hit = layer._cache["recip"] = (rkey, smoothing_reciprocal(s))
+    qa = quant_act_smoothed(x, s, check=check, recip=hit[1])
+    qw = layer.qweights
+    fused = layer_fused_scales(layer)
+    run = w4a8_gemm_per_channel if qw.scheme == PER_CHANNEL else w4a8_gemm_per_group
+    return run(qa, qw, fused, with_acc=False).y_wide()

@@ -77,25 +77,44 @@ def shard_ksplit(qw: QuantizedWeights, rank: int, world: int) -> QuantizedWeight
 
 
 class TPOps:
-    """Per-rank compute of the TP layers, on the sm_100a library."""
+    """Per-rank compute of the TP layers, on the sm_100a library.
+
+    check=True raises DataError for non-finite activations at once (a host
+    sync per call, like the reference); check=False (serving / benchmarking)
+    ORs the error bits into the per-device deferred status word instead, so a
+    layer's launches and collectives stay asynchronous (and graph-capturable);
+    `quantize.raise_if_bad(quantize.deferred_status(dev))` reports them later.
+    """
+
+    def __init__(self, check: bool = True):
+        self.check = check
+
+    def _status(self, dev):
+        from .quantize import deferred_status
+
+        return torch.zeros(1, dtype=torch.int32, device=dev) if self.check else deferred_status(dev)
+
+    def _raise(self, status):
+        if self.check:
+            from .quantize import raise_if_bad
+
+            raise_if_bad(status, "activations")
 
     def quant(self, x) -> QuantizedActivations:
         from .quantize import quant_act_per_token
 
-        return quant_act_per_token(x)
+        return quant_act_per_token(x, check=self.check)
 
     def row_absmax(self, x: torch.Tensor) -> torch.Tensor:
         x = as_cuda(x).contiguous()
         m, k = x.shape
         lib = _lib.lib_for_device(x.device)
         out = torch.empty(m, dtype=torch.float64, device=x.device)
-        status = torch.zeros(1, dtype=torch.int32, device=x.device)
+        status = self._status(x.device)
         dt = {torch.float16: 0, torch.float32: 1, torch.float64: 2}[x.dtype]
         _lib.check(lib.qqq_act_absmax(_lib.ptr(x), dt, m, k, k, _lib.ptr(out), _lib.ptr(status),
                                       _lib.stream_of(x.device)), "act_absmax")
-        from .quantize import raise_if_bad
-
-        raise_if_bad(status, "activations")
+        self._raise(status)
         return out
 
     def quant_with_max(self, x: torch.Tensor, row_max: torch.Tensor) -> QuantizedActivations:
@@ -106,7 +125,7 @@ class TPOps:
         q = torch.empty((m, kp), dtype=torch.int8, device=x.device)
         s_a = torch.empty(m, dtype=torch.float64, device=x.device)
         rowsum = torch.empty(m, dtype=torch.int32, device=x.device)
-        status = torch.zeros(1, dtype=torch.int32, device=x.device)
+        status = self._status(x.device)
         dt = {torch.float16: 0, torch.float32: 1, torch.float64: 2}[x.dtype]
         _lib.check(lib.qqq_act_quant_with_max(_lib.ptr(x), dt, m, k, k, _lib.ptr(row_max.contiguous()), _lib.ptr(q),
                                               kp, _lib.ptr(s_a), _lib.ptr(rowsum), _lib.ptr(status),

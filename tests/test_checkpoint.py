@@ -133,7 +133,7 @@ def test_gpu_load_reference_layers_bit_exact(tmp_path):
     layers = load_layers(CKPT)
     assert set(layers) == {"blk0.qkv", "blk0.down"}
     for name, layer in layers.items():
-        assert layer.qweights.packed.is_cuda and layer._cache.get("fused") is not None
+        assert layer.qweights.packed.is_cuda and layer._cache.get("fused") is not None  # (key, FusedScales)
         y = Q.apply_quant_linear(torch.from_numpy(exp[f"{name}.x"]).cuda(), layer)
         assert np.array_equal(y.cpu().numpy().view(np.uint64), exp[f"{name}.y"].view(np.uint64)), name
     # store -> write -> read: the same bytes as the reference wrote
