@@ -546,6 +546,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       if (++wi == C::kWStages) wi = 0;
     }
     griddep_wait();  // the int8 activations come from the previous kernel
+    if (lane == 0) QQQ_STAMP(3);
     for (int i = 0; i < C::kXStages && i < total; ++i) issue_x();
     uint32_t ws = 0, wph = 0, xs = 0, xph = 0;
 #pragma unroll 1
