@@ -75,6 +75,10 @@ QQQ_DEVICE void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+QQQ_DEVICE void mbar_arrive_addr(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+
 QQQ_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
@@ -323,14 +327,21 @@ QQQ_DEVICE void mma_commit(uint64_t* bar) {
 
 QQQ_DEVICE void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// 32 lanes x 32-bit, 16 consecutive columns per thread
+// 32 lanes x 32-bit, 16 consecutive columns per thread, and the wait for the
+// load in the SAME asm statement. tcgen05.ld writes its destination registers
+// asynchronously (they are valid only after tcgen05.wait::ld); as two asm
+// statements the compiler may copy or spill the outputs between them — it did
+// once register pressure rose (64-register half-SM CTAs), storing garbage for
+// the 32-token cluster split-K partials.
 QQQ_DEVICE void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
+      : "r"(taddr)
+      : "memory");
 }
 
 // Shared-memory matrix descriptor (tcgen05 "version 1" format).

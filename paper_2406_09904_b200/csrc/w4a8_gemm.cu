@@ -43,6 +43,7 @@ namespace qqq {
 constexpr int kDbgSlots = 192;
 #endif
 
+
 struct GemmParams {
   const uint8_t* w;     // repacked weight blob (qqq_layout.cuh)
   const double* s_a;    // [M]
@@ -110,10 +111,14 @@ struct Cfg {
   static constexpr int kConvWarp0 = 0;
   static constexpr int kEpiWarp0 = kNumConvWarps;
   // big CTA: TMEM allocator, activation producer, weight producer and MMA warps;
-  // small CTA: one producer warp for both rings, and the MMA warp allocates TMEM
+  // small CTA: the MMA warp allocates TMEM. Weights and activations have their
+  // own producer warps in both: the weight ring keeps streaming (and the
+  // converters keep filling TMEM A buffers) while the activation producer sits
+  // in the PDL wait, so a decode CTA has all the k-blocks the rings hold
+  // loaded, and kABufs of them converted, before the previous kernel finishes.
   static constexpr int kAllocWarp = kEpiWarp0 + kNumEpiWarps;
-  static constexpr int kActProducerWarp = kSmall ? kAllocWarp + 1 : kAllocWarp + 1;
-  static constexpr int kWProducerWarp = kSmall ? kAllocWarp + 1 : kAllocWarp + 2;
+  static constexpr int kActProducerWarp = kAllocWarp + 1;
+  static constexpr int kWProducerWarp = kAllocWarp + 2;
   static constexpr int kMmaWarp = kSmall ? kAllocWarp : kAllocWarp + 3;
   static constexpr int kNumThreads = ((kSmall ? kWProducerWarp : kMmaWarp) + 1) * 32;
   static constexpr int kSmemBudget = kSmall ? 111 * 1024 : 225 * 1024;
@@ -149,7 +154,10 @@ struct Cfg {
 #ifndef QQQ_PAIR_WMAX
 #define QQQ_PAIR_WMAX 12
 #endif
-  static constexpr int kXCapWanted = PAIR ? QQQ_PAIR_XCAP : 4;
+#ifndef QQQ_SMALL_XCAP
+#define QQQ_SMALL_XCAP 4
+#endif
+  static constexpr int kXCapWanted = PAIR ? QQQ_PAIR_XCAP : kSmall ? QQQ_SMALL_XCAP : 4;
   static constexpr int kXCap = kABufsMax < kXCapWanted ? kABufsMax : kXCapWanted;
   static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > kXCap ? kXCap : kXStagesRaw);
   static constexpr int kABufs = kConvert ? kXStages : 0;
@@ -328,10 +336,14 @@ QQQ_DEVICE void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" :::
 // A CTA's work: up to two contiguous (tile, k-block) unit ranges, iterated in
 // order and split at tile borders: [u, u1) then [v, v1) (hybrid plans: whole
 // data-parallel tiles first, then the stream-K share).
+// (32-bit unit indices: units = tiles x k-blocks < 65536 x 512. Every warp
+// role keeps an iterator live across its whole loop; 64-bit state was spilled
+// to local memory, and a spill reload after a long barrier wait missed L1 and
+// cost an L2 round trip on the decode critical path.)
 struct SegIter {
-  int64_t u, u1, v, v1;
+  int u, u1, v, v1;
   int kbt;
-  QQQ_DEVICE int64_t total() const { return (u1 - u) + (v1 - v); }
+  QQQ_DEVICE int total() const { return (u1 - u) + (v1 - v); }
   QQQ_DEVICE bool next(int& tile, int& kb0, int& kb1) {
     if (u >= u1) {
       if (v >= v1) return false;
@@ -339,10 +351,10 @@ struct SegIter {
       u1 = v1;
       v = v1;
     }
-    tile = (int)(u / kbt);
-    kb0 = (int)(u % kbt);
-    const int64_t rem = u1 - u;
-    kb1 = (int)((kbt - kb0) < rem ? kbt : kb0 + rem);
+    tile = u / kbt;
+    kb0 = u - tile * kbt;
+    const int rem = u1 - u;
+    kb1 = (kbt - kb0) < rem ? kbt : kb0 + rem;
     u += kb1 - kb0;
     return true;
   }
@@ -354,8 +366,8 @@ QQQ_DEVICE SegIter make_iter(const GemmParams& p) {
   it.v = it.v1 = 0;
   if (p.csplit > 1) {  // cluster split-K: one tile per cluster, an even k-range per rank
     const int c = blockIdx.x / p.csplit, r = blockIdx.x % p.csplit;
-    it.u = (int64_t)c * p.kb_per_tile + r * p.kb_per_tile / p.csplit;
-    it.u1 = (int64_t)c * p.kb_per_tile + (r + 1) * p.kb_per_tile / p.csplit;
+    it.u = c * p.kb_per_tile + r * p.kb_per_tile / p.csplit;
+    it.u1 = c * p.kb_per_tile + (r + 1) * p.kb_per_tile / p.csplit;
     return it;
   }
   if (p.aligned_tiles > 0) {
@@ -365,18 +377,18 @@ QQQ_DEVICE SegIter make_iter(const GemmParams& p) {
     int64_t t1 = t0 + p.aligned_tiles < tiles ? t0 + p.aligned_tiles : tiles;
     if (t0 > tiles) t0 = tiles;
     if (t1 < t0) t1 = t0;
-    it.u = t0 * p.kb_per_tile;
-    it.u1 = t1 * p.kb_per_tile;
+    it.u = (int)(t0 * p.kb_per_tile);
+    it.u1 = (int)(t1 * p.kb_per_tile);
   } else {
     // (pair plans: the stream-K "CTA" is the CTA pair; both CTAs take the same units)
     const int64_t b = p.pair ? blockIdx.x >> 1 : blockIdx.x, G = p.pair ? gridDim.x >> 1 : gridDim.x;
-    it.u = p.sk_unit0 + b * p.units / G;
-    it.u1 = p.sk_unit0 + (b + 1) * p.units / G;
+    it.u = (int)(p.sk_unit0 + b * p.units / G);
+    it.u1 = (int)(p.sk_unit0 + (b + 1) * p.units / G);
     if (p.dp_tiles > 0) {
       it.v = it.u;
       it.v1 = it.u1;
-      it.u = b * p.dp_tiles * p.kb_per_tile;
-      it.u1 = it.u + (int64_t)p.dp_tiles * p.kb_per_tile;
+      it.u = (int)(b * p.dp_tiles * p.kb_per_tile);
+      it.u1 = it.u + p.dp_tiles * p.kb_per_tile;
     }
   }
   return it;
@@ -453,6 +465,13 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
 
   if (threadIdx.x == 0) {
     QQQ_STAMP(0);
+#ifdef QQQ_TIMELINE
+    if (p.dbg) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      p.dbg[(size_t)blockIdx.x * kDbgSlots + 191] = smid;
+    }
+#endif
     griddep_launch_dependents();
     for (int s = 0; s < C::kXStages; ++s) {
       mbar_init(&kb_full[s], C::kConvert ? (PAIR ? 2 : 1) * C::kConvPerGroup + 1 : 1);
@@ -514,86 +533,35 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
   // then warp-uniform and live in uniform registers. Issuing tcgen05.mma from
   // a divergent single lane costs ~150 cycles per MMA (R2UR waterfall,
   // scripts/mma_probe.cu) against a 16-cycle issue floor at N = 16.
-  if (C::kSmall && warp == C::kWProducerWarp) {
-    // ========== producer warp (small CTA): weight + activation rings ==========
-    // One in-order loop over this CTA's k-blocks i = 0..total-1: the weight
-    // stage of k-block i is refilled (k-block i + kWStages) once the
-    // converters released it, the activation slot of k-block i once its MMAs
-    // retired. The weight prologue is issued before the PDL wait (weights
-    // never depend on the previous kernel).
-    SegIter si = make_iter(p);
-    const int total = (int)si.total();  // small CTAs: a single stream-K range (no data-parallel part)
-    UnitCursor wc(p, si.u), xc = wc;
-    uint32_t wi = 0, xi = 0;  // ring slots of the next copies
-    auto issue_w = [&]() {
-      if (elect_one()) issue_weight_kblock<BK>(p, wc, smem + C::kOffW + wi * C::kWBytes, &w_full[wi]);
-      __syncwarp();
-      wc.adv(p);
-      if (++wi == C::kWStages) wi = 0;
-    };
-    auto issue_x = [&]() {
-      if (elect_one()) {
-        mbar_arrive_expect_tx(&kb_full[xi], C::kXBytes);
-        tma_load_3d(smem + C::kOffX + xi * C::kXBytes, &act_map, 0, xc.tt * NTOK, xc.kb * (BK / 128), &kb_full[xi]);
-      }
-      __syncwarp();
-      xc.adv(p);
-      if (++xi == C::kXStages) xi = 0;
-    };
-    // the weight prologue was issued before the set-up barrier: advance past it
-    for (int i = 0; i < C::kWStages && i < total; ++i) {
-      wc.adv(p);
-      if (++wi == C::kWStages) wi = 0;
-    }
-    griddep_wait();  // the int8 activations come from the previous kernel
-    if (lane == 0) QQQ_STAMP(3);
-    for (int i = 0; i < C::kXStages && i < total; ++i) issue_x();
-    uint32_t ws = 0, wph = 0, xs = 0, xph = 0;
-#pragma unroll 1
-    for (int i = 0; i < total; ++i) {
-      if (i + C::kWStages < total) {
-        mbar_wait_sleep(&w_empty[ws], wph);
-        issue_w();
-      }
-      if (++ws == C::kWStages) {
-        ws = 0;
-        wph ^= 1;
-      }
-      if (i + C::kXStages < total) {
-        mbar_wait_sleep(&kb_empty[xs], xph);
-        issue_x();
-        if (lane == 0 && i < 16) QQQ_STAMP(112 + i);
-      }
-      if (++xs == C::kXStages) {
-        xs = 0;
-        xph ^= 1;
-      }
-    }
-  } else if (!C::kSmall && warp == C::kWProducerWarp) {  // big CTA
+  if (warp == C::kWProducerWarp) {
     // ===================== weight producer (bulk copies) =====================
     // Weights never depend on the previous kernel in the stream: no PDL wait,
-    // so under PDL they stream in while the previous kernel drains.
+    // so under PDL they stream in while the previous kernel drains. (Small
+    // CTAs issued the first kWStages k-blocks before the set-up barrier.)
     if (lane == 0) QQQ_STAMP(1);
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
-    uint32_t s = 0, ph = 0;
+    uint32_t s = 0, ph = 0, i = 0;
+    const uint32_t pre = C::kSmall ? (uint32_t)(si.total() < C::kWStages ? si.total() : C::kWStages) : 0u;
     while (si.next(tile, kb0, kb1)) {
       // (pair mode, odd channel-tile count: the missing last tile converts a copy of
       //  a real one; its rows are never stored)
       const int n_tile = min(ntile_of(tile), p.n_tiles - 1);
 #pragma unroll 1
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait_sleep(&w_empty[s], ph ^ 1);
-        if (elect_one()) {
-          // the last k-block of a tile may hold fewer super-slabs (K_pad % BK != 0):
-          // the stale rest of the stage meets zero-filled (OOB) activations
-          const int nss = min(BK / 128, p.ss_per_tile - kb * (BK / 128));
-          const uint32_t wbytes = (uint32_t)(nss * p.ss_bytes);
-          mbar_arrive_expect_tx(&w_full[s], wbytes);
-          const int64_t ss0 = (int64_t)n_tile * p.ss_per_tile + (int64_t)kb * (BK / 128);
-          bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &w_full[s]);
+      for (int kb = kb0; kb < kb1; ++kb, ++i) {
+        if (i >= pre) {
+          mbar_wait_sleep(&w_empty[s], ph ^ 1);
+          if (elect_one()) {
+            // the last k-block of a tile may hold fewer super-slabs (K_pad % BK != 0):
+            // the stale rest of the stage meets zero-filled (OOB) activations
+            const int nss = min(BK / 128, p.ss_per_tile - kb * (BK / 128));
+            const uint32_t wbytes = (uint32_t)(nss * p.ss_bytes);
+            mbar_arrive_expect_tx(&w_full[s], wbytes);
+            const int64_t ss0 = (int64_t)n_tile * p.ss_per_tile + (int64_t)kb * (BK / 128);
+            bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &w_full[s]);
+          }
+          __syncwarp();
         }
-        __syncwarp();
         if (++s == C::kWStages) {
           s = 0;
           ph ^= 1;
@@ -601,7 +569,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       }
     }
     if (lane == 0) QQQ_STAMP(2);
-  } else if (!C::kSmall && warp == C::kActProducerWarp) {
+  } else if (warp == C::kActProducerWarp) {
     // ================== activation producer (3-D tensor TMA) ==================
     griddep_wait();  // the int8 activations come from the previous kernel
     if (lane == 0) QQQ_STAMP(3);
@@ -716,6 +684,9 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     // Warp w owns TMEM lane quadrant q = w % 4 (rows 32q..32q+31) and every
     // other 32-k slab (parity w / 4): thread = one output channel.
     if constexpr (C::kConvert) {
+#ifdef QQQ_EXP_CONV_AFTER_WAIT
+      griddep_wait();  // experiment: no conversion while the previous kernel runs
+#endif
       constexpr int kPhases = C::kConvPerGroup / 4;
       const int q = warp & 3, h = (warp >> 2) % kPhases;  // quadrant, slab phase (0..kPhases-1)
       const int grp = (warp >> 2) / kPhases;               // k-block interleaving group
@@ -772,16 +743,28 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             }
           }
           // Release the packed stage as soon as its bytes are in registers (before
-          // the conversion), so the producer refills it one conversion earlier:
-          // the asm consumes the last shared loads (LDS complete in order per
-          // warp), which makes every lane wait for its loads before the arrive.
+          // the conversion), so the producer refills it one conversion earlier.
+          // The arrive must not issue before the loads have RETURNED (an empty asm
+          // consuming a register emits no instruction, so it does not wait): fold
+          // the last word of every slab (and the scales) into a zero offset of the
+          // barrier address, which makes the arrive data-dependent on every load.
           {
-            uint32_t dep = v[kSlabs - 1].w;
-            if constexpr (MODE == kModePG) dep ^= s1[kSlabs - 1];
-            asm volatile("" ::"r"(dep));
+            uint32_t dep = 0;
+#pragma unroll
+            for (int i = 0; i < kSlabs; ++i) {
+              dep ^= v[i].w;
+              if constexpr (MODE == kModePG) dep ^= s1[i];
+            }
+            asm volatile("and.b32 %0, %0, 0;" : "+r"(dep));
+            // one arrive per warp (the loads are one instruction per slab for the
+            // whole warp, so lane 0's data dependency covers every lane).
+            // (Per-lane arrives with a 32x arrival count were measured to complete
+            // the phase early — stages refilled under the readers — so the
+            // warp-level release stays; compute-sanitizer racecheck reports this
+            // lane-0-after-__syncwarp release as a WAR hazard on lanes 1..31.)
+            __syncwarp();
+            if (lane == 0) mbar_arrive_addr(smem_u32(&w_empty[ws]) + dep);
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&w_empty[ws]);
           if (++ws == C::kWStages) {
             ws = 0;
             wph ^= 1;
@@ -809,6 +792,9 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             }
           }
           conv_wait(&kb_empty[ab], aph ^ 1);
+          // the wait loop exits per lane: reconverge before the .sync.aligned
+          // tcgen05.st / wait::st (a divergent warp there corrupted A buffers)
+          __syncwarp();
           tc_fence_after();
           if (stamp_warp && lane == 0 && it < 16) QQQ_STAMP(64 + it);
           const uint32_t abase = a_lane + ab * C::kACols;
@@ -816,6 +802,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
 #pragma unroll
           for (int i = 0; i < kSlabs; ++i) tmem_st8(abase + kPhases * i * 8, o[i]);
           tmem_wait_st();
+          // keep the source registers of the asynchronous stores live (unreused)
+          // until tcgen05.wait::st has returned
+#pragma unroll
+          for (int i = 0; i < kSlabs; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) asm volatile("" ::"r"(o[i][j]));
 #else
           if (o[0][0] == 0x12345678u && o[kSlabs - 1][7] == 0x9abcdef0u) tmem_st8(abase, o[0]);
 #endif
@@ -845,13 +837,27 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     // own TMEM accumulator (exact integer sum) and applies the dequant. All
     // CTAs of the grid are co-resident (grid <= #SMs), so the wait cannot
     // deadlock, and it is normally already satisfied.
-    griddep_wait();  // y / acc / workspace / counters / s_a may belong to the previous kernel
     // two halves of 4 warps (each covering all 128 TMEM lanes) take alternate
     // 16-token chunks: half the per-thread work, same TMEM/partial/y protocol
     constexpr int H = C::kEpiGroups;
     const int eh = (warp - C::kEpiWarp0) >> 2;
     const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = q * 32 + lane;
+    // The first segment's column scale is weight metadata (never written by the
+    // previous kernel, like the weights): load it before the PDL wait so the
+    // decode epilogue does not pay a cold HBM round trip after the MMAs.
+    int n_first = -1;
+    double s_col_first = 0.0;
+    {
+      SegIter pk = make_iter(p);
+      int t_, a_, b_;
+      if (pk.next(t_, a_, b_)) {
+        n_first = ntile_of(t_) * 128 + row;
+        if (n_first < p.N && p.s_col)
+          asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(s_col_first) : "l"(p.s_col + n_first));
+      }
+    }
+    griddep_wait();  // y / acc / workspace / counters / s_a may belong to the previous kernel
     const int et = threadIdx.x - C::kEpiWarp0 * 32;  // 0..kAll-1
     const bool lead = et == 0;                    // segment-level lead (counters)
     const bool hlead = (et & 127) == 0;           // half lead (TMA stores, partial prefetch)
@@ -888,7 +894,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
 #else
       const bool whole = cs || (kb0 == 0 && kb1 == p.kb_per_tile);
 #endif
-      const double s_col = (n_ok && p.s_col) ? p.s_col[n] : 0.0;
+      const double s_col = n == n_first ? s_col_first : (n_ok && p.s_col) ? p.s_col[n] : 0.0;
       int seg_idx = 0, nsegs = 1;
       int32_t* slots = nullptr;
       // pair plans: segments are counted in CTA pairs; each CTA of a pair reduces its
@@ -942,14 +948,14 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
 #pragma unroll
         for (int c0 = 0; c0 < NTOK; c0 += 16) {
           uint32_t r[16];
-          tmem_ld16(taddr + c0, r);
-          tmem_wait_ld();
+          tmem_ld16(taddr + c0, r);  // (includes tcgen05.wait::ld)
 #pragma unroll
           for (int i = 0; i < 16; ++i) own[c0 + i] = r[i];
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[j]);
+        if (lead) QQQ_STAMP(150);
         if (dest != me) {
           const uint32_t dst = mapa_shared(recv + (me * rows_per + (row - drow0)) * NTOK, (uint32_t)dest);
           const uint32_t dbar = mapa_shared(&part_full[0], (uint32_t)dest);
@@ -957,6 +963,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           for (int i = 0; i < NTOK; i += 4) st_async_v4(dst + i * 4, own[i], own[i + 1], own[i + 2], own[i + 3], dbar);
         } else {
           mbar_wait(&part_full[0], seg & 1);
+          if (lead) QQQ_STAMP(151);
           const int lr = row - drow0;
 #pragma unroll 1
           for (int sg = 0; sg < S; ++sg) {
@@ -965,6 +972,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
 #pragma unroll
             for (int i = 0; i < NTOK; ++i) own[i] += (uint32_t)src[i];
           }
+          if (lead) QQQ_STAMP(152);
           if (n_ok) {
 #pragma unroll
             for (int c0 = 0; c0 < NTOK; c0 += 16) {
@@ -991,6 +999,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           }
         }
         }  // NTOK <= 32
+        if (lead) QQQ_STAMP(153);
         if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
         ++seg;
         continue;
@@ -1004,8 +1013,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
         for (int li = 0; li < nmine; ++li) {
           const int c0 = (eh + H * li) * 16;
           uint32_t r[16];
-          tmem_ld16(taddr + c0, r);
-          tmem_wait_ld();
+          tmem_ld16(taddr + c0, r);  // (includes tcgen05.wait::ld)
           if (tvalid - c0 < 4) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
@@ -1087,8 +1095,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
         for (int li = 0; li < nmine; ++li) {
           const int c0 = (eh + H * li) * 16;
           uint32_t r[16];
-          tmem_ld16(taddr + c0, r);
-          tmem_wait_ld();
+          tmem_ld16(taddr + c0, r);  // (includes tcgen05.wait::ld)
           if (lead && seg == 0 && li < 16) QQQ_STAMP(44 + li);
           if (!whole) {
             const uint32_t pc = pchunk + li;
@@ -1141,6 +1148,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
       ++seg;
     }
+    if (lead) QQQ_STAMP(154);
     if (lane == 0) bulk_wait_read<0>();  // y stores have read their staging before the CTA retires
     if (lead) QQQ_STAMP(63);
   }
@@ -1153,6 +1161,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
   } else {
     __syncthreads();
   }
+  if (threadIdx.x == 0) QQQ_STAMP(42);
   if (warp == C::kAllocWarp) {
     tc_fence_after();
     if constexpr (PAIR)
@@ -1218,7 +1227,10 @@ struct LaunchPlan {
 #ifndef QQQ_BIG_BK
 #define QQQ_BIG_BK 256
 #endif
-static constexpr int bk_for(int mode, int ntok) { return ntok <= 64 ? 256 : mode == kModeI8 ? 128 : QQQ_BIG_BK; }
+#ifndef QQQ_SMALL_BK
+#define QQQ_SMALL_BK 256
+#endif
+static constexpr int bk_for(int mode, int ntok) { return ntok <= 64 ? QQQ_SMALL_BK : mode == kModeI8 ? 128 : QQQ_BIG_BK; }
 static constexpr int ctas_per_sm(int mode, int ntok) { return ntok <= 64 && mode != kModeI8 ? 2 : 1; }
 #ifndef QQQ_PAIR_BK
 #define QQQ_PAIR_BK 128
@@ -1581,7 +1593,7 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
 
   LaunchPlan lp = make_plan(mode, M, N, K, cfg ? cfg->ntok : 0, cfg ? cfg->grid : 0, cfg ? cfg->split : -1,
                             cfg ? cfg->csplit : 0);
-  if (lp.tiles * (lp.pair ? 2 : 1) > kMaxTiles) return kErrUnsupported;
+  if (lp.tiles * (lp.pair ? 2 : 1) > kMaxTiles || lp.units > 0x7fffffff) return kErrUnsupported;
   if (ws_bytes < plan_ws_bytes(lp)) return kErrConfig;
 
   CUtensorMap map;

@@ -69,7 +69,7 @@ print(f"{a.shape} M={a.m} {a.scheme} plan={info} chain={L} graph {s.elapsed_time
 ds = [d.cpu().numpy().astype(np.int64) for d in dbgs]
 t0 = min(d[d[:, 0] > 0, 0].min() for d in ds)
 SLOTS = [("start", 0), ("dep_wait", 3), ("full0", 4), ("conv0", 80), ("mma_xfull0", 96), ("mma0", 20),
-         ("accfull0", 36), ("epi_end", 63)]
+         ("accfull0", 36), ("cs_own", 150), ("cs_recv", 151), ("cs_add", 152), ("cs_done", 153), ("loop_end", 154), ("epi_end", 63), ("exit", 42)]
 
 
 def stat(d, sl):
@@ -86,5 +86,18 @@ ends = []
 for i, d in enumerate(ds):
     d = d[d[:, 0] > 0]
     print(f"{i:6d}  {len(d):4d}  " + "  ".join(f"{stat(d, sl):>20s}" for _, sl in SLOTS))
-    ends.append((d[:, 63][d[:, 63] > 0].max() - t0) / 1e3)
-print("epilogue-end deltas (us):", " ".join(f"{ends[i] - ends[i - 1]:.2f}" for i in range(1, L)))
+    ends.append((d[:, 42][d[:, 42] > 0].max() - t0) / 1e3)
+print("last-CTA-exit deltas (us):", " ".join(f"{ends[i] - ends[i - 1]:.2f}" for i in range(1, L)))
+# the 6 latest-exiting CTAs of the middle launch: every stamp, and the SM they ran on
+mid = ds[L // 2]
+mid = mid[mid[:, 0] > 0]
+order = np.argsort(-mid[:, 42])
+print(f"launch {L // 2}: latest-exiting CTAs (sm, then us per stamp)")
+for r in order[:6]:
+    print(f"  sm={int(mid[r, 191]):3d} " + " ".join(f"{nm}={(mid[r, sl] - t0) / 1e3:.2f}" for nm, sl in SLOTS if mid[r, sl] > 0))
+# SM sharing: how many CTAs of launches L//2-1 and L//2+1 ran on the same SMs as the latest CTAs
+for j in (L // 2 - 1, L // 2 + 1):
+    o = ds[j][ds[j][:, 0] > 0]
+    sms = set(int(v) for v in o[:, 191])
+    print(f"  launch {j}: {len(o)} CTAs on {len(sms)} SMs; latest-6 SMs shared: "
+          f"{sum(int(mid[r, 191]) in sms for r in order[:6])}/6")
