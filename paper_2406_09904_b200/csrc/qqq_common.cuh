@@ -148,6 +148,11 @@ QQQ_DEVICE uint32_t mapa_shared(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+QQQ_DEVICE uint32_t mapa_shared_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
 // Arrive on a barrier of another CTA of the cluster. Default (.release.cta)
 // semantics: a .cluster-scope release compiles to MEMBAR.ALL.GPU, which under a
 // streaming HBM load costs ~0.9 us per arrive (measured); the data it guards
@@ -337,11 +342,16 @@ QQQ_DEVICE void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+#ifndef QQQ_EXP_SPLITLD
       "tcgen05.wait::ld.sync.aligned;"
+#endif
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr)
       : "memory");
+#ifdef QQQ_EXP_SPLITLD
+  tmem_wait_ld();
+#endif
 }
 
 // Shared-memory matrix descriptor (tcgen05 "version 1" format).

@@ -117,8 +117,13 @@ struct Cfg {
   // in the PDL wait, so a decode CTA has all the k-blocks the rings hold
   // loaded, and kABufs of them converted, before the previous kernel finishes.
   static constexpr int kAllocWarp = kEpiWarp0 + kNumEpiWarps;
+#ifdef QQQ_SMALL_ONE_PRODUCER
+  static constexpr int kActProducerWarp = kAllocWarp + 1;
+  static constexpr int kWProducerWarp = kSmall ? kAllocWarp + 1 : kAllocWarp + 2;
+#else
   static constexpr int kActProducerWarp = kAllocWarp + 1;
   static constexpr int kWProducerWarp = kAllocWarp + 2;
+#endif
   static constexpr int kMmaWarp = kSmall ? kAllocWarp : kAllocWarp + 3;
   static constexpr int kNumThreads = ((kSmall ? kWProducerWarp : kMmaWarp) + 1) * 32;
   static constexpr int kSmemBudget = kSmall ? 111 * 1024 : 225 * 1024;
@@ -518,10 +523,15 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     }
   }
   tc_fence_before();
+  // The TMEM base address (written to shared memory by tcgen05.alloc) and the
+  // barrier inits are published to the CTA by bar.sync. The cluster barrier
+  // below uses a RELAXED arrive (a .release arrive is a per-thread MEMBAR.GPU),
+  // which orders nothing: with it alone, warps of cluster CTAs read a stale
+  // tmem_slot now and then (left by the SM's previous CTA) and converted into
+  // another CTA's TMEM columns.
+  __syncthreads();
   if (PAIR || p.csplit > 1)
     cluster_sync_all();  // every cluster CTA's barriers initialised before any remote arrive / store
-  else
-    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // the even CTA's k-block-full and accumulator-empty barriers (pair mode)
@@ -533,6 +543,63 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
   // then warp-uniform and live in uniform registers. Issuing tcgen05.mma from
   // a divergent single lane costs ~150 cycles per MMA (R2UR waterfall,
   // scripts/mma_probe.cu) against a 16-cycle issue floor at N = 16.
+#ifdef QQQ_SMALL_ONE_PRODUCER
+  if (C::kSmall && warp == C::kWProducerWarp) {
+    // ========== producer warp (small CTA): weight + activation rings ==========
+    // One in-order loop over this CTA's k-blocks i = 0..total-1: the weight
+    // stage of k-block i is refilled (k-block i + kWStages) once the
+    // converters released it, the activation slot of k-block i once its MMAs
+    // retired. The weight prologue is issued before the PDL wait (weights
+    // never depend on the previous kernel).
+    SegIter si = make_iter(p);
+    const int total = (int)si.total();  // small CTAs: a single stream-K range (no data-parallel part)
+    UnitCursor wc(p, si.u), xc = wc;
+    uint32_t wi = 0, xi = 0;  // ring slots of the next copies
+    auto issue_w = [&]() {
+      if (elect_one()) issue_weight_kblock<BK>(p, wc, smem + C::kOffW + wi * C::kWBytes, &w_full[wi]);
+      __syncwarp();
+      wc.adv(p);
+      if (++wi == C::kWStages) wi = 0;
+    };
+    auto issue_x = [&]() {
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&kb_full[xi], C::kXBytes);
+        tma_load_3d(smem + C::kOffX + xi * C::kXBytes, &act_map, 0, xc.tt * NTOK, xc.kb * (BK / 128), &kb_full[xi]);
+      }
+      __syncwarp();
+      xc.adv(p);
+      if (++xi == C::kXStages) xi = 0;
+    };
+    // the weight prologue was issued before the set-up barrier: advance past it
+    for (int i = 0; i < C::kWStages && i < total; ++i) {
+      wc.adv(p);
+      if (++wi == C::kWStages) wi = 0;
+    }
+    griddep_wait();  // the int8 activations come from the previous kernel
+    for (int i = 0; i < C::kXStages && i < total; ++i) issue_x();
+    uint32_t ws = 0, wph = 0, xs = 0, xph = 0;
+#pragma unroll 1
+    for (int i = 0; i < total; ++i) {
+      if (i + C::kWStages < total) {
+        mbar_wait_sleep(&w_empty[ws], wph);
+        issue_w();
+      }
+      if (++ws == C::kWStages) {
+        ws = 0;
+        wph ^= 1;
+      }
+      if (i + C::kXStages < total) {
+        mbar_wait_sleep(&kb_empty[xs], xph);
+        issue_x();
+        if (lane == 0 && i < 16) QQQ_STAMP(112 + i);
+      }
+      if (++xs == C::kXStages) {
+        xs = 0;
+        xph ^= 1;
+      }
+    }
+  } else
+#endif
   if (warp == C::kWProducerWarp) {
     // ===================== weight producer (bulk copies) =====================
     // Weights never depend on the previous kernel in the stream: no PDL wait,
@@ -541,8 +608,9 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     if (lane == 0) QQQ_STAMP(1);
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
-    uint32_t s = 0, ph = 0, i = 0;
-    const uint32_t pre = C::kSmall ? (uint32_t)(si.total() < C::kWStages ? si.total() : C::kWStages) : 0u;
+    uint32_t s = 0, ph = 0;
+    int i = 0;
+    const int pre = C::kSmall ? (si.total() < C::kWStages ? si.total() : C::kWStages) : 0;
     while (si.next(tile, kb0, kb1)) {
       // (pair mode, odd channel-tile count: the missing last tile converts a copy of
       //  a real one; its rows are never stored)
@@ -755,7 +823,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
               dep ^= v[i].w;
               if constexpr (MODE == kModePG) dep ^= s1[i];
             }
+#ifdef QQQ_EXP_NODEP
+            asm volatile("" ::"r"(dep));
+            dep = 0;
+#else
             asm volatile("and.b32 %0, %0, 0;" : "+r"(dep));
+#endif
             // one arrive per warp (the loads are one instruction per slab for the
             // whole warp, so lane 0's data dependency covers every lane).
             // (Per-lane arrives with a 32x arrival count were measured to complete
@@ -793,8 +866,10 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           }
           conv_wait(&kb_empty[ab], aph ^ 1);
           // the wait loop exits per lane: reconverge before the .sync.aligned
-          // tcgen05.st / wait::st (a divergent warp there corrupted A buffers)
+          // tcgen05.st / wait::st
+#ifndef QQQ_EXP_NOSYNC
           __syncwarp();
+#endif
           tc_fence_after();
           if (stamp_warp && lane == 0 && it < 16) QQQ_STAMP(64 + it);
           const uint32_t abase = a_lane + ab * C::kACols;
@@ -804,10 +879,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           tmem_wait_st();
           // keep the source registers of the asynchronous stores live (unreused)
           // until tcgen05.wait::st has returned
+#ifndef QQQ_EXP_NOKEEP
 #pragma unroll
           for (int i = 0; i < kSlabs; ++i)
 #pragma unroll
             for (int j = 0; j < 8; ++j) asm volatile("" ::"r"(o[i][j]));
+#endif
 #else
           if (o[0][0] == 0x12345678u && o[kSlabs - 1][7] == 0x9abcdef0u) tmem_st8(abase, o[0]);
 #endif
@@ -853,8 +930,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       int t_, a_, b_;
       if (pk.next(t_, a_, b_)) {
         n_first = ntile_of(t_) * 128 + row;
+#ifndef QQQ_EXP_NOSCOL
         if (n_first < p.N && p.s_col)
           asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(s_col_first) : "l"(p.s_col + n_first));
+#else
+        n_first = -1;
+#endif
       }
     }
     griddep_wait();  // y / acc / workspace / counters / s_a may belong to the previous kernel
@@ -889,10 +970,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       const int n = n_tile * 128 + row;
       const bool n_ok = n < p.N;
       const bool cs = C::kSmall && p.csplit > 1;  // cluster split-K: DSMEM reduce-scatter below
+      // big-CTA cluster split-K (128-token tiles): reduce-scatter by TOKEN range
+      const bool csb = !C::kSmall && !PAIR && NTOK == 128 && p.csplit > 1;
 #ifdef QQQ_EXP_NO_FIXUP
       const bool whole = true;  // experiment: every segment stores its own partial (wrong results)
 #else
-      const bool whole = cs || (kb0 == 0 && kb1 == p.kb_per_tile);
+      const bool whole = cs || csb || (kb0 == 0 && kb1 == p.kb_per_tile);
 #endif
       const double s_col = n == n_first ? s_col_first : (n_ok && p.s_col) ? p.s_col[n] : 0.0;
       int seg_idx = 0, nsegs = 1;
@@ -917,6 +1000,16 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
         const int S = p.csplit, me = (int)cluster_ctarank();
         const int mine = ((me + 1) * 128 + S - 1) / S - (me * 128 + S - 1) / S;
         mbar_arrive_expect_tx(&part_full[0], (uint32_t)((S - 1) * mine * NTOK * 4));
+      }
+      if (csb && lead) {
+        // this CTA finalizes tokens [me*T, (me+1)*T) of all 128 channels (T = NTOK/S):
+        // the other S-1 ranks each send those tokens' int32 partials, 16-token chunk
+        // by chunk (only chunks holding valid tokens)
+        const int S = p.csplit, me = (int)cluster_ctarank(), T = NTOK / S;
+        int nvc = 0;
+        for (int c0 = me * T; c0 < (me + 1) * T; c0 += 16) nvc += c0 < tvalid ? 1 : 0;
+        if (nvc) mbar_arrive_expect_tx(&part_full[0], (uint32_t)((S - 1) * nvc * 16 * 128 * 4));
+        else mbar_arrive(&part_full[0]);
       }
       // ONE warp polls the accumulator barrier (backoff), the others block in a
       // named barrier: with every epilogue warp polling, the polls were ~40% of
@@ -952,6 +1045,23 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
 #pragma unroll
           for (int i = 0; i < 16; ++i) own[c0 + i] = r[i];
         }
+#ifdef QQQ_DBG_PARTIALS
+        if (p.dbg) {  // debug build: every CTA's own partial [cta][128 rows][NTOK], and a re-read 4 us later
+          int32_t* d = reinterpret_cast<int32_t*>(p.dbg) + ((size_t)blockIdx.x * 128 + row) * NTOK;
+#pragma unroll
+          for (int i = 0; i < NTOK; ++i) d[i] = (int32_t)own[i];
+          const unsigned long long t0 = gtimer();
+          while (gtimer() - t0 < 4000) __nanosleep(200);
+          int32_t* d2 = d + (size_t)gridDim.x * 128 * NTOK;
+#pragma unroll
+          for (int c0 = 0; c0 < NTOK; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(taddr + c0, r);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) d2[c0 + i] = (int32_t)r[i];
+          }
+        }
+#endif
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[j]);
@@ -1003,6 +1113,91 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
         if (lead && seg < 4) QQQ_STAMP(37 + 2 * seg);
         ++seg;
         continue;
+      }
+      if constexpr (!C::kSmall && !PAIR && NTOK == 128) {
+        if (csb) {
+          // ---- big-CTA cluster split-K: reduce-scatter the int32 partials over
+          // DSMEM by token range. Rank me finalizes tokens [me*T, (me+1)*T) for all
+          // 128 channel rows, so every epilogue warp (each TMEM lane quadrant) takes
+          // part. Receive layout (one slot per peer, in rank order without me):
+          // [slot][chunk of 16 tokens][4 token quads][128 rows][4 int32]: one
+          // st.async.v4 of a warp writes 512 contiguous bytes.
+          const int S = p.csplit, me = (int)cluster_ctarank(), T = NTOK / S, CPR = T / 16;
+          int32_t* recv = reinterpret_cast<int32_t*>(smem + C::kOffPart);
+          const uint32_t recv_cl0 = smem_u32(recv);
+          const uint32_t pbar = smem_u32(&part_full[0]);
+          // phase 1: send every valid chunk owned by another rank (this group's chunks)
+#pragma unroll 1
+          for (int li = 0; li < nmine; ++li) {
+            const int c = eh + H * li, c0 = c * 16;
+            const int d = c0 / T;
+            if (d == me) continue;
+            uint32_t r[16];
+            tmem_ld16(taddr + c0, r);  // (includes tcgen05.wait::ld)
+            const int slot = me < d ? me : me - 1;
+            const uint32_t off = (uint32_t)((((slot * CPR + (c - d * CPR)) * 4) * 128 + row) * 16);
+            const uint32_t dst = mapa_shared_u32(recv_cl0 + off, (uint32_t)d);
+            const uint32_t dbar = mapa_shared_u32(pbar, (uint32_t)d);
+#pragma unroll
+            for (int t4 = 0; t4 < 4; ++t4)
+              st_async_v4(dst + t4 * 128 * 16, r[4 * t4], r[4 * t4 + 1], r[4 * t4 + 2], r[4 * t4 + 3], dbar);
+          }
+          if (lead) QQQ_STAMP(150);
+          // phase 2: own token range: own partial (TMEM) + the S-1 received ones
+          bool waited = false;
+#pragma unroll 1
+          for (int li = 0; li < nmine; ++li) {
+            const int c = eh + H * li, c0 = c * 16;
+            if (c0 / T != me) continue;
+            if (!waited) {
+              mbar_wait(&part_full[0], seg & 1);
+              waited = true;
+              if (lead) QQQ_STAMP(151);
+            }
+            uint32_t r[16];
+            tmem_ld16(taddr + c0, r);
+#pragma unroll 1
+            for (int slot = 0; slot < S - 1; ++slot) {
+              const int4* src = reinterpret_cast<const int4*>(recv) + ((slot * CPR + (c - me * CPR)) * 4) * 128 + row;
+#pragma unroll
+              for (int t4 = 0; t4 < 4; ++t4) {
+                const int4 v = src[t4 * 128];
+                r[4 * t4] += (uint32_t)v.x;
+                r[4 * t4 + 1] += (uint32_t)v.y;
+                r[4 * t4 + 2] += (uint32_t)v.z;
+                r[4 * t4 + 3] += (uint32_t)v.w;
+              }
+            }
+            if constexpr (C::kU8) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) r[i] -= (uint32_t)rs_smem[c0 + i];  // u8 weights carried +128
+            }
+            store_outputs(p, r, sa_smem + c0, tok0 + c0, tvalid - c0, n, n_ok, s_col);
+            if (p.y_tma) {
+              uint16_t* stg = reinterpret_cast<uint16_t*>(ystage) + (ych & 1) * 512;
+              uint16_t h[16];
+              dequant16(r, sa_smem + c0, s_col, h, tvalid - c0);
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) stg[i * 32 + lane] = h[i];
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&y_map, stg, n_tile * 128 + q * 32, tok0 + c0);
+                bulk_commit();
+              }
+              ++ych;
+            }
+          }
+          if (!waited && lead) mbar_wait(&part_full[0], seg & 1);  // (keep the barrier phase in step)
+          if (lead) QQQ_STAMP(153);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[j]);
+          ++seg;
+          continue;
+        }
       }
       if (!owner) {
         // ---- contributor: add the partial into the tile's slot, release the counter.
@@ -1157,8 +1352,10 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     // no CTA of the cluster retires while another may still signal its barriers,
     // store into its shared memory or (pair) read its shared memory / TMEM
     tc_fence_before();
+    __syncthreads();  // (CTA-scope ordering of the TMEM reads before the dealloc; the relaxed cluster barrier has none)
     cluster_sync_all();
   } else {
+    tc_fence_before();
     __syncthreads();
   }
   if (threadIdx.x == 0) QQQ_STAMP(42);
@@ -1282,6 +1479,35 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
   // cluster split-K: decode tiles only (NTOK 16/32, 2 CTAs per SM). (A 128-token
   // prefill variant — 64 KiB partials over DSMEM — measured slower than stream-K:
   // the exchange ran at ~7 B/clk per SM.)
+  if (split == 4 && ntok == 128 && mode != kModeI8) {
+    // big-CTA cluster split-K (128-token tiles): one tile per cluster of S in {2, 4}
+    // whole-SM CTAs, partials reduce-scattered by token range over DSMEM (the
+    // receive buffer, (S-1) x 128/S tokens x 128 rows x 4 B, is the 48 KiB partial
+    // ring). For mid M on few channel tiles (4096x4096: 32 tiles for 148 SMs).
+    lp.ntok = ntok;
+    lp.bk = bk_for(mode, ntok);
+    lp.tok_tiles = (int)((M + ntok - 1) / ntok);
+    lp.n_tiles = (int)(round_up(N, kTileN) / kTileN);
+    lp.kb_per_tile = (int)((round_up(K, kKPadTo) + lp.bk - 1) / lp.bk);
+    lp.tiles = lp.n_tiles * lp.tok_tiles;
+    lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
+    lp.max_segs = 1;
+    const int slots = force_grid > 0 ? std::min(force_grid, num_sms()) : num_sms();
+    int S = 1;
+    if ((force_cs == 2 || force_cs == 4) && force_cs <= lp.kb_per_tile) {
+      S = force_cs;
+    } else {
+      for (int c : {4, 2})
+        if ((int64_t)lp.tiles * c <= slots && c <= lp.kb_per_tile) {
+          S = c;
+          break;
+        }
+    }
+    if (S == 1) return plan_for(mode, M, N, K, ntok, 1, force_grid);
+    lp.csplit = S;
+    lp.grid = lp.tiles * S;
+    return lp;
+  }
   if (split == 4 && (ntok > 32 || ctas_per_sm(mode, ntok) != 2)) split = 1;
   if (split == 4) {
     // cluster split-K: one tile per cluster of S decode CTAs: the largest S that
@@ -1294,7 +1520,12 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
     lp.tiles = lp.n_tiles * lp.tok_tiles;
     lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
     lp.max_segs = 1;
-    const int slots = (force_grid > 0 ? std::min(force_grid, num_sms()) : num_sms()) * ctas_per_sm(mode, ntok);
+    // 32-token clusters are kept to one CTA per SM: with two co-resident 32-token
+    // cluster CTAs per SM, stress runs (scripts/stress_plans.py, 800 launches)
+    // saw one TMEM lane quadrant of one CTA's partial corrupted in 1-10% of the
+    // launches (never with one CTA per SM, never with 16-token clusters).
+    const int slots = (force_grid > 0 ? std::min(force_grid, num_sms()) : num_sms()) *
+                      (ntok == 32 ? 1 : ctas_per_sm(mode, ntok));
     // Cluster size S <= 8 (portable), receive buffer [S][ceil(128/S)][NTOK] int32
     // within the 16 KiB partial ring (every S for NTOK=16, divisors of 128 for
     // 32). Measured (profiles/r01_csplit_size_sweep.txt): the fastest S is the
@@ -1424,6 +1655,13 @@ static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
   const double u = std::max(std::max(wkb / bw, conv), mma);
   const double mt = (double)std::min<int64_t>(lp.ntok, M) / 16.0;
   const double epi = kE0 + kE1 * mt;
+  if (lp.csplit > 1 && lp.ntok == 128) {
+    // big-CTA cluster split-K: the per-CTA k-blocks at the 1-CTA/SM pace plus the
+    // DSMEM exchange ((S-1)/S x 64 KiB at ~15 B/clk) and the epilogue
+    const double ucta_cs = (double)((lp.kb_per_tile + lp.csplit - 1) / lp.csplit);
+    const double xchg = (lp.csplit - 1.0) / lp.csplit * 65536.0 / 15.0 / clk;
+    return T0 + ucta_cs * u + xchg + epi;
+  }
   if (lp.csplit > 1) {
     // cluster split-K (linear fit to profiles/r01_csplit_sweep.jsonl, 7% rms): a
     // fixed cost, the per-CTA k-blocks, a penalty for the k-blocks of CTAs that
@@ -1457,7 +1695,8 @@ static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force
     if (nt > 32 && nt / 4 >= M) break;  // a smaller tile already covers every token
     // whole tiles / stream-K / pair tiles / cluster split-K (the hybrid never won a sweep point)
     for (int sk = 0; sk < 5; ++sk) {
-      if (sk == 2 || (sk == 3 && (nt != 256 || mode == kModeI8)) || (sk == 4 && (nt > 32 || mode == kModeI8)))
+      if (sk == 2 || (sk == 3 && (nt != 256 || mode == kModeI8)) ||
+          (sk == 4 && ((nt > 32 && nt != 128) || mode == kModeI8)))
         continue;
       const LaunchPlan lp = plan_for(mode, M, N, K, nt, sk, 0);
       if (lp.tiles > 65536) continue;
@@ -1489,15 +1728,17 @@ static int launch_t(const CUtensorMap& map, const CUtensorMap& ymap, const GemmP
   auto kern = w4a8_gemm_kernel<MODE, NTOK, BK, PAIR>;
   static bool attr_set[kMaxDevices] = {};  // per instantiation and device
   const int dev = cur_device();
+  static const int one_per_sm = getenv("QQQ_EXP_ONE_CTA_PER_SM") ? 1 : 0;  // developer A/B switch
+  const int smem_bytes = (one_per_sm && C::kSmall) ? 150 * 1024 : C::kSmemBytes;
   if (!attr_set[dev]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess)
       return kErrCuda;
     attr_set[dev] = true;
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(grid);
   lc.blockDim = dim3(C::kNumThreads);
-  lc.dynamicSmemBytes = C::kSmemBytes;
+  lc.dynamicSmemBytes = smem_bytes;
   lc.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

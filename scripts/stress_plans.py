@@ -26,6 +26,7 @@ ap.add_argument("--reps", type=int, default=200)
 ap.add_argument("--scheme", default="per-group")
 ap.add_argument("--cfgs", default="auto")
 ap.add_argument("--interleave", action="store_true", help="alternate the plans launch by launch (PDL overlap)")
+ap.add_argument("--requant", action="store_true", help="re-run the activation quantizer before every GEMM")
 a = ap.parse_args()
 k, n = map(int, a.shape.split("x"))
 rng = np.random.default_rng(7)
@@ -53,6 +54,8 @@ order = [(r, i) for r in range(a.reps) for i in range(len(cfgs))] if a.interleav
     [(r, i) for i in range(len(cfgs)) for r in range(a.reps)]
 pending = []
 for r, i in order:
+    if a.requant:
+        aq = Q.quant_act_per_token(x)
     out = G.run_gemm(aq, prep, n, True, cfg=cfgs[i])
     pending.append((i, out))
     if len(pending) >= 16:
@@ -60,6 +63,14 @@ for r, i in order:
         for j, o in pending:
             if not (torch.equal(o.acc, want_acc) and torch.equal(o.y.view(torch.int16), want_y)):
                 bad[j] += 1
+                if bad[j] <= 3:
+                    d = (o.acc.long() - want_acc.long()).cpu().numpy()
+                    cols = np.nonzero(d.any(0))[0]
+                    tiles = sorted(set((cols // 128).tolist()))
+                    rows = sorted(set((cols % 128).tolist()))
+                    print(f"  mismatch cfg={cfgs[j]}: {cols.size} cols, tiles {tiles[:12]}, rows-in-tile "
+                          f"{rows[:40]}{'...' if len(rows) > 40 else ''}; diff sample {d[0, cols[:6]].tolist()}",
+                          flush=True)
         pending = []
 torch.cuda.synchronize()
 for j, o in pending:

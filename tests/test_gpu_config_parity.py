@@ -116,10 +116,10 @@ def candidate_plans(mode, m, n, k):
         if nt > 32 and nt // 4 >= m:
             break
         for sk in (0, 1, 3, 4):
-            if (sk == 3 and nt != 256) or (sk == 4 and nt > 32):
+            if (sk == 3 and nt != 256) or (sk == 4 and nt > 32 and nt != 128):
                 continue
             if sk == 4:
-                for s in range(2, 9):
+                for s in (range(2, 9) if nt <= 32 else (2, 4)):
                     add({"ntok": nt, "split": 4, "csplit": s})
             else:
                 add({"ntok": nt, "split": sk})

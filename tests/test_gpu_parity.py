@@ -323,6 +323,32 @@ def test_gemm_cluster_splitk(scheme, gs, ntok):
             assert same_bits(out.y, want.y), (scheme, gs, ntok, m, k, n)
 
 
+@pytest.mark.parametrize("scheme,gs", [("per-channel", 0), ("per-group", 128), ("per-group", 32)])
+@pytest.mark.parametrize("cs", [2, 4])
+def test_gemm_cluster_splitk_128_token_tiles(scheme, gs, cs):
+    """Big-CTA cluster split-K (128-token tiles, S in {2, 4} whole-SM CTAs, int32
+    partials reduce-scattered over DSMEM by token range): ragged M (token ranges
+    with no valid token, partial 16-token chunks), several token tiles, partial
+    last k-block, both schemes; a second launch leaves no state behind."""
+    for (m, k, n) in ((1, 4096, 4096), (16, 2048, 1280), (33, 2304, 384), (64, 4096, 4096), (100, 1024, 640),
+                      (128, 4352, 256), (129, 2048, 512), (300, 1792, 1280), (512, 4096, 4096)):
+        x16, qw_o = _rand_problem(m, k, n, scheme, gs or 128, seed=m * 3 + k + n)
+        aq_o = O.quant_act_per_token(x16.astype(np.float64))
+        run_o = O.w4a8_gemm_per_channel if scheme == "per-channel" else O.w4a8_gemm_per_group
+        want = run_o(aq_o, qw_o, O.FusedScales.from_quantized(qw_o), fast=True)
+        qw = _to_gpu_qw(qw_o)
+        prep = Q.gemm.prepare(qw, Q.FusedScales.from_quantized(qw))
+        aq = Q.quant_act_per_token(torch.from_numpy(x16).cuda())
+        cfg = {"ntok": 128, "split": 4, "csplit": cs}
+        info = Q.gemm.plan_info(prep.mode, m, n, k, cfg)
+        for _ in range(2):
+            out = Q.gemm.run_gemm(aq, prep, n, True, cfg=cfg)
+            assert same_bits(out.acc, want.acc), (scheme, gs, cs, m, k, n, info)
+            assert same_bits(out.y, want.y), (scheme, gs, cs, m, k, n, info)
+        y_only = Q.gemm.run_gemm(aq, prep, n, False, cfg=cfg)  # the serving path (TMA y stores, no acc)
+        assert same_bits(y_only.y, want.y), (scheme, gs, cs, m, k, n, info, "no-acc")
+
+
 def test_gemm_plans_share_a_zeroed_workspace():
     """Every plan leaves the shared split-K workspace zeroed (counters re-armed,
     slots returned to zero): a chain of GEMMs of different shapes and plans —
