@@ -161,6 +161,32 @@ QQQ_DEVICE uint32_t mapa_shared_u32(uint32_t saddr, uint32_t rank) {
 QQQ_DEVICE void mbar_arrive_cluster(uint32_t cl_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
 }
+// parity wait with an explicit cluster-scope ACQUIRE: data published by peer
+// CTAs (global-memory stores, fence.acq_rel.gpu, remote arrive) is visible after it
+QQQ_DEVICE void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  unsigned long long t0 = 0;
+#pragma unroll 1
+  for (uint32_t n = 0;; ++n) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity), "r"(0x100000u)
+        : "memory");
+    if (done) return;
+#ifndef QQQ_NO_WATCHDOG
+    if ((n & 255) == 255) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) __trap();
+    }
+#endif
+  }
+}
 // parity wait with cluster-scope acquire (arrivals come from the peer CTA too)
 QQQ_DEVICE void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);

@@ -43,6 +43,16 @@ namespace qqq {
 constexpr int kDbgSlots = 192;
 #endif
 
+// Big-CTA cluster split-K partial exchange: through DSMEM st.async (default), or
+// through L2 (QQQ_CSB_L2=1: coalesced stores to per-(tile, destination, sender)
+// workspace chunks, one gpu-scope fence + remote arrive per CTA, cluster-scope
+// acquire). Measured: the L2 exchange is 0.4-0.9 us slower per GEMM on
+// 4096x4096 / 11008x4096 at M = 32-256 (the fence and the L2 round trips cost
+// more than DSMEM's ~20 B/clk), so DSMEM stays.
+#ifndef QQQ_CSB_L2
+#define QQQ_CSB_L2 0
+#endif
+
 
 struct GemmParams {
   const uint8_t* w;     // repacked weight blob (qqq_layout.cuh)
@@ -492,7 +502,8 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       mbar_init(&acc_full[j], 1);
       mbar_init(&acc_empty[j], (PAIR ? 2 : 1) * C::kNumEpiWarps);
     }
-    for (int i = 0; i < 2 * C::kEpiGroups; ++i) mbar_init(&part_full[i], 1);
+    for (int i = 0; i < 2 * C::kEpiGroups; ++i)  // (big-CTA cluster split-K, L2 exchange: part_full[1] counts the S-1 peers)
+      mbar_init(&part_full[i], (QQQ_CSB_L2 && i == 1 && !C::kSmall && !PAIR && NTOK == 128 && p.csplit > 1) ? p.csplit - 1 : 1);
     mbar_fence_init();
   }
   if (warp == C::kActProducerWarp && lane == 0) tma_prefetch_desc(&act_map);
@@ -1001,7 +1012,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
         const int mine = ((me + 1) * 128 + S - 1) / S - (me * 128 + S - 1) / S;
         mbar_arrive_expect_tx(&part_full[0], (uint32_t)((S - 1) * mine * NTOK * 4));
       }
-      if (csb && lead) {
+      if (!QQQ_CSB_L2 && csb && lead) {
         // this CTA finalizes tokens [me*T, (me+1)*T) of all 128 channels (T = NTOK/S):
         // the other S-1 ranks each send those tokens' int32 partials, 16-token chunk
         // by chunk (only chunks holding valid tokens)
@@ -1127,6 +1138,32 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           const uint32_t recv_cl0 = smem_u32(recv);
           const uint32_t pbar = smem_u32(&part_full[0]);
           // phase 1: send every valid chunk owned by another rank (this group's chunks)
+#if QQQ_CSB_L2
+          // workspace chunk (tile, dest d, sender slot j, chunk cc): [4 token quads][128 rows][4 int32]
+          auto ws_chunk = [&](int d, int jslot, int cc) -> int4* {
+            return reinterpret_cast<int4*>(p.ws + ((((size_t)tile * S + d) * (S - 1) + jslot) * CPR + cc) * 2048);
+          };
+#pragma unroll 1
+          for (int li = 0; li < nmine; ++li) {
+            const int c = eh + H * li, c0 = c * 16;
+            const int d = c0 / T;
+            if (d == me) continue;
+            uint32_t r[16];
+            tmem_ld16(taddr + c0, r);  // (includes tcgen05.wait::ld)
+            int4* dst = ws_chunk(d, me < d ? me : me - 1, c - d * CPR) + row;
+#pragma unroll
+            for (int t4 = 0; t4 < 4; ++t4)
+              __stcg(dst + t4 * 128, make_int4((int)r[4 * t4], (int)r[4 * t4 + 1], (int)r[4 * t4 + 2], (int)r[4 * t4 + 3]));
+          }
+          // publish: every epilogue thread's stores, then ONE gpu-scope fence and a
+          // remote arrive on each peer's part_full[1] (count S-1)
+          named_bar_sync(kBarAll, kAll);
+          if (lead) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            for (int d = 0; d < S; ++d)
+              if (d != me) mbar_arrive_cluster(mapa_shared(&part_full[1], (uint32_t)d));
+          }
+#else
 #pragma unroll 1
           for (int li = 0; li < nmine; ++li) {
             const int c = eh + H * li, c0 = c * 16;
@@ -1142,6 +1179,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             for (int t4 = 0; t4 < 4; ++t4)
               st_async_v4(dst + t4 * 128 * 16, r[4 * t4], r[4 * t4 + 1], r[4 * t4 + 2], r[4 * t4 + 3], dbar);
           }
+#endif
           if (lead) QQQ_STAMP(150);
           // phase 2: own token range: own partial (TMEM) + the S-1 received ones
           bool waited = false;
@@ -1150,7 +1188,11 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             const int c = eh + H * li, c0 = c * 16;
             if (c0 / T != me) continue;
             if (!waited) {
+#if QQQ_CSB_L2
+              mbar_wait_acq_cluster(&part_full[1], seg & 1);
+#else
               mbar_wait(&part_full[0], seg & 1);
+#endif
               waited = true;
               if (lead) QQQ_STAMP(151);
             }
@@ -1158,10 +1200,18 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             tmem_ld16(taddr + c0, r);
 #pragma unroll 1
             for (int slot = 0; slot < S - 1; ++slot) {
+#if QQQ_CSB_L2
+              const int4* src = ws_chunk(me, slot, c - me * CPR) + row;
+#else
               const int4* src = reinterpret_cast<const int4*>(recv) + ((slot * CPR + (c - me * CPR)) * 4) * 128 + row;
+#endif
 #pragma unroll
               for (int t4 = 0; t4 < 4; ++t4) {
+#if QQQ_CSB_L2
+                const int4 v = __ldcg(src + t4 * 128);
+#else
                 const int4 v = src[t4 * 128];
+#endif
                 r[4 * t4] += (uint32_t)v.x;
                 r[4 * t4 + 1] += (uint32_t)v.y;
                 r[4 * t4 + 2] += (uint32_t)v.z;
@@ -1190,7 +1240,9 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
               ++ych;
             }
           }
+#if !QQQ_CSB_L2
           if (!waited && lead) mbar_wait(&part_full[0], seg & 1);  // (keep the barrier phase in step)
+#endif
           if (lead) QQQ_STAMP(153);
           tc_fence_before();
           __syncwarp();
@@ -1716,6 +1768,8 @@ constexpr int kMaxTiles = 65536;
 constexpr size_t kCounterBytes = (size_t)kMaxTiles * 4;
 
 static size_t plan_ws_bytes(const LaunchPlan& lp) {
+  if (QQQ_CSB_L2 && lp.csplit > 1 && lp.ntok == 128)  // (S-1) received partials per tile, 64 KiB each
+    return kCounterBytes + (size_t)lp.tiles * (lp.csplit - 1) * lp.ntok * 128 * 4;
   if (lp.aligned_tiles > 0 || lp.csplit > 1) return kCounterBytes;
   if (lp.pair) return kCounterBytes + (size_t)lp.tiles * 2 * lp.ntok * 128 * 4;  // a slot per (pair tile, CTA)
   return kCounterBytes + (size_t)lp.tiles * lp.ntok * 128 * 4;
@@ -1789,6 +1843,10 @@ extern "C" size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   }
   {
     LaunchPlan lp = plan_for(kModePG, M, N, K, 256, 5, 0);  // pair stream-K: a slot per (pair tile, CTA)
+    best = std::max(best, plan_ws_bytes(lp));
+  }
+  for (int cs : {2, 4}) {  // 128-token clusters (partials exchanged through the workspace)
+    LaunchPlan lp = plan_for(kModePG, M, N, K, 128, 4, 0, cs);
     best = std::max(best, plan_ws_bytes(lp));
   }
   return best;

@@ -1,10 +1,3 @@
-run() { echo "== $2" >> gpurun_out/stress.txt; timeout 300 python scripts/stress_plans.py --shape $1 --m $3 --reps 800 --requant --scheme $4 --cfgs "$2" 2>&1 | grep -v "^  mismatch" >> gpurun_out/stress.txt; }
-run 11008x4096 auto 1 per-group
-run 4096x11008 auto 1 per-group
-run 4096x11008 auto 16 per-channel
-run 8192x28672 '{"ntok":16,"split":4,"csplit":2}' 16 per-group
-run 11008x4096 '{"ntok":32,"split":1}' 32 per-group
-run 4096x11008 auto 32 per-group
-cat gpurun_out/stress.txt
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu_1.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu_1.log
-tail -2 gpurun_out/pytest_gpu_1.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_stress.py -q -x -p no:cacheprovider -k "cluster_splitk_128 or repeated" > gpurun_out/pytest_q.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_q.log
+tail -3 gpurun_out/pytest_q.log
+LIBS="prod csbdsmem" QB="--shapes 4096x4096,11008x4096 --ms 32,64,128,256 --cfgs auto;{\"ntok\":128,\"split\":4,\"csplit\":2};{\"ntok\":128,\"split\":4,\"csplit\":4}" bash scripts/gpu_abq.sh
