@@ -886,9 +886,21 @@ def run_c5(args, world, rank, dev, peaks, summary_only=False):
         torch.cuda.synchronize()
         return max_over_ranks(s.elapsed_time(e) * 1e3 / reps, world)
 
+    # Device time per call: the rank's launches (and NCCL collectives) captured in
+    # one CUDA graph over the R cold replicas; eager (host-launch-bound for these
+    # microsecond kernels) only where capture is unavailable (gloo).
+    def timed(fn, reps):
+        if args.dist_backend != "gloo":
+            try:
+                t = graph_time_us([(lambda i: (lambda: fn(i)))(i) for i in range(R)], reps=max(2, reps // R), dev=dev)
+                return max_over_ranks(t, world), "cuda graph"
+            except Exception:  # (capture unsupported here: fall back to eager launches)
+                torch.cuda.synchronize()
+        return timed_eager(fn, reps), "eager"
+
     breakdown = []
     for (L, m) in order:
-        t_layer = timed_eager(lambda i: call(L, m, i), 2 * R)
+        t_layer, how = timed(lambda i: call(L, m, i), 4 * R)
         t_comm = 0.0
         if world > 1 and L["split"] == "k":
             nb = torch.empty((m, L["n"]), dtype=torch.int32, device=dev)
@@ -898,9 +910,9 @@ def run_c5(args, world, rank, dev, peaks, summary_only=False):
                 dist.all_reduce(mx, op=dist.ReduceOp.MAX)
                 dist.all_reduce(nb, op=dist.ReduceOp.SUM)
 
-            t_comm = timed_eager(comm, 10)
+            t_comm, _ = timed(comm, 10)
         ops_full = 2.0 * m * L["k"] * L["n"]
-        breakdown.append(dict(layer=L["name"], split=L["split"], M=m, us=round(t_layer, 2),
+        breakdown.append(dict(layer=L["name"], split=L["split"], M=m, us=round(t_layer, 2), timing=how,
                               comm_us=round(t_comm, 2), gemm_us=round(max(t_layer - t_comm, 0.0), 2),
                               TOPS=round(ops_full / (t_layer * 1e-6) / 1e12, 2),
                               allreduce_bytes=(4 * m * L["n"] + 8 * m) if L["split"] == "k" else 0))
@@ -910,9 +922,27 @@ def run_c5(args, world, rank, dev, peaks, summary_only=False):
         for (L, m) in order:
             call(L, m, i)
 
-    # the step: eager (NCCL collectives between our launches), K timed steps
+    # the step (every layer at every M, NCCL collectives between our launches),
+    # captured once as a CUDA graph (eager where capture is unavailable); K timed steps
     for i in range(max(args.warmup, 3)):
         step(i)
+    torch.cuda.synchronize()
+    run_step, step_mode = step, "eager"
+    if args.dist_backend != "gloo":
+        try:
+            graphs = []
+            for r in range(R):  # one graph per cold replica: step i replays graph i % R
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=capture_stream(dev)):
+                    step(r)
+                graphs.append(g)
+            graphs[0].replay()
+            torch.cuda.synchronize()
+            run_step, step_mode = (lambda i: graphs[i % R].replay()), "cuda graph"
+        except Exception:
+            torch.cuda.synchronize()
+    for i in range(max(args.warmup, 3)):
+        run_step(i)
     barrier(world)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clk_summary = None
@@ -920,7 +950,7 @@ def run_c5(args, world, rank, dev, peaks, summary_only=False):
         barrier(world)
         s.record()
         for i in range(args.steps):
-            step(i)
+            run_step(i)
         e.record()
         torch.cuda.synchronize()
         barrier(world)
@@ -928,7 +958,7 @@ def run_c5(args, world, rank, dev, peaks, summary_only=False):
     elapsed_ms = max_over_ranks(s.elapsed_time(e), world)
     value = ops_step * args.steps / (elapsed_ms * 1e-3) / 1e12
     out = dict(value=round(value, 3), unit="TOPS", n_gpus=world, ms_per_step=round(elapsed_ms / args.steps, 4),
-               tp_parity_vs_1gpu=ok, layers=breakdown, clocks=clk_summary, ops_step=ops_step,
+               tp_parity_vs_1gpu=ok, layers=breakdown, clocks=clk_summary, ops_step=ops_step, step_mode=step_mode,
                l2=f"{R} rotated shard replicas per rank ({R * per_rank_bytes / 2**20:.0f} MB)")
     if summary_only:
         return out

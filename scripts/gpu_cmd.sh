@@ -1,3 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_stress.py -q -x -p no:cacheprovider -k "cluster_splitk_128 or repeated" > gpurun_out/pytest_q.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_q.log
-tail -3 gpurun_out/pytest_q.log
-LIBS="prod csbdsmem" QB="--shapes 4096x4096,11008x4096 --ms 32,64,128,256 --cfgs auto;{\"ntok\":128,\"split\":4,\"csplit\":2};{\"ntok\":128,\"split\":4,\"csplit\":4}" bash scripts/gpu_abq.sh
+timeout 900 python -m pytest tests/test_pipeline.py tests/test_gpu_parity.py -q -p no:cacheprovider -k "smooth or pipeline or quant or markstein or apply" > gpurun_out/pytest_q.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_q.log
+tail -3 gpurun_out/pytest_q.log; grep FAILED gpurun_out/pytest_q.log
+timeout 600 python scripts/c4_probe.py > gpurun_out/c4_probe.txt 2>&1; cat gpurun_out/c4_probe.txt
