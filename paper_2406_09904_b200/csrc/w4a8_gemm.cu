@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     w4a8_gemm_kernel(const __grid_constant__ CUtensorMap act_map, const __grid_constant__ CUtensorMap y_map,
                      const GemmParams p) {
   using C = Cfg<MODE, NTOK, BK, PAIR>;
-  static_assert(!PAIR || (C::kConvert && !C::kSmall && C::kAccBufs == 1), "pair mode: prefill convert tiles");
+  static_assert(!PAIR || (C::kConvert && !C::kSmall), "pair mode: prefill convert tiles");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
@@ -1604,7 +1604,7 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
     return lp;
   }
   const bool pair_plan = split == 3 || split == 5 || split == 6;
-  if (pair_plan && (ntok != 256 || mode == kModeI8)) split = split == 3 ? 0 : split == 5 ? 1 : 2;
+  if (pair_plan && ((ntok != 256 && ntok != 192) || mode == kModeI8)) split = split == 3 ? 0 : split == 5 ? 1 : 2;
   if (split == 3 || split == 5 || split == 6) {
     // pair tiles: 3 = whole pair tiles, 5 = stream-K over (pair tile, k-block) units
     // across the CTA pairs, 6 = whole-tile waves + the remainder stream-K'd
@@ -1723,9 +1723,13 @@ static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
     return 4.813 + 0.456 * ucta_cs + 0.671 * shared * ucta_cs + (lp.ntok == 32 ? 2.229 : 0.0) + 0.012 * mt;
   }
   if (lp.pair) {
-    // 2-CTA pair tiles: ~0.41 us per 128-deep k-block of a 256x256 pair tile
+    // 2-CTA pair tiles: ~0.41 us per 128-deep k-block of a 256x256 pair tile; the
+    // 192-token pair tile double-buffers its accumulator, so only the last tile's
+    // epilogue is exposed (per-k-block time scaled by the MMA width, 192/256)
     const double kT0p = 1.41, kUp = 0.4133;
-    return kT0p + (double)lp.aligned_tiles * lp.kb_per_tile * kUp + lp.aligned_tiles * epi;
+    const double tiles_pp = lp.aligned_tiles > 0 ? (double)lp.aligned_tiles : (double)lp.units / lp.kb_per_tile / (lp.grid / 2);
+    if (lp.ntok == 192) return kT0p + tiles_pp * lp.kb_per_tile * kUp * 0.78 + epi;
+    return kT0p + tiles_pp * lp.kb_per_tile * kUp + tiles_pp * epi;
   }
   if (lp.aligned_tiles > 0) return T0 + ucta * u + lp.aligned_tiles * epi;
   return T0 + ucta * u + kF0 + kF1 * mt + epi;
@@ -1743,8 +1747,23 @@ static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force
   // NTOK=64 stays available by config but is not auto-selected: as a half-SM
   // CTA it only fits 2 weight + 2 activation stages, and the NTOK=128 plan
   // measured faster at every M it would cover (r01_tileplan_sweep_v2)
-  for (int nt : {16, 32, 128, 256}) {
+  for (int nt : {16, 32, 128, 192, 256}) {
     if (nt > 32 && nt / 4 >= M) break;  // a smaller tile already covers every token
+    if (nt == 192) {
+      // 192-token pair tiles (double-buffered accumulators) stay a forced-plan option:
+      // measured slower than the 256-token pair tile wherever it would be picked
+      // (4096x11008 M=1024 54.3 vs 51.8 us, 11008x4096 66.3 vs 38.3 us): prefill is
+      // co-bound by the INT4->INT8 conversion, which a 192-token tile repeats for
+      // 6 instead of 4 token tiles at M = 1024, more than the hidden epilogue saves.
+      if (mode == kModeI8 || !getenv("QQQ_EXP_AUTO_192")) continue;
+      const LaunchPlan lp = plan_for(mode, M, N, K, nt, 3, 0);
+      const double t = plan_cost_us(lp, M);
+      if (lp.tiles <= 65536 && t < best_t) {
+        best_t = t;
+        best = lp;
+      }
+      continue;
+    }
     // whole tiles / stream-K / pair tiles / cluster split-K (the hybrid never won a sweep point)
     for (int sk = 0; sk < 5; ++sk) {
       if (sk == 2 || (sk == 3 && (nt != 256 || mode == kModeI8)) ||
@@ -1821,10 +1840,12 @@ static int launch_mode(int ntok, const CUtensorMap& map, const CUtensorMap& ymap
 }
 
 template <int MODE>
-static int launch_pair(const CUtensorMap& map, const CUtensorMap& ymap, const GemmParams& p, int grid,
+static int launch_pair(int ntok, const CUtensorMap& map, const CUtensorMap& ymap, const GemmParams& p, int grid,
                        cudaStream_t st) {
   if constexpr (MODE == kModeI8)
     return kErrConfig;
+  else if (ntok == 192)  // double-buffered accumulators (2 x 192 + 4 A buffers of 32 TMEM columns)
+    return launch_t<MODE, 192, kPairBk, true>(map, ymap, p, grid, st);
   else
     return launch_t<MODE, 256, kPairBk, true>(map, ymap, p, grid, st);
 }
@@ -1841,8 +1862,8 @@ extern "C" size_t qqq_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K) {
     size_t b = plan_ws_bytes(lp);
     if (b > best) best = b;
   }
-  {
-    LaunchPlan lp = plan_for(kModePG, M, N, K, 256, 5, 0);  // pair stream-K: a slot per (pair tile, CTA)
+  for (int nt : {192, 256}) {
+    LaunchPlan lp = plan_for(kModePG, M, N, K, nt, 5, 0);  // pair stream-K: a slot per (pair tile, CTA)
     best = std::max(best, plan_ws_bytes(lp));
   }
   for (int cs : {2, 4}) {  // 128-token clusters (partials exchanged through the workspace)
@@ -1957,8 +1978,8 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
 
   if (lp.pair) {
     switch (mode) {
-      case kModePC: return launch_pair<kModePC>(map, ymap, p, lp.grid, stream);
-      case kModePG: return launch_pair<kModePG>(map, ymap, p, lp.grid, stream);
+      case kModePC: return launch_pair<kModePC>(lp.ntok, map, ymap, p, lp.grid, stream);
+      case kModePG: return launch_pair<kModePG>(lp.ntok, map, ymap, p, lp.grid, stream);
       default: return kErrConfig;
     }
   }

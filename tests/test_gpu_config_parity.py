@@ -112,9 +112,13 @@ def candidate_plans(mode, m, n, k):
             out.append((cfg, info))
 
     add(None)
-    for nt in (16, 32, 128, 256):
+    for nt in (16, 32, 128, 192, 256):
         if nt > 32 and nt // 4 >= m:
             break
+        if nt == 192:  # pair tiles only (whole tiles, stream-K, waves + stream-K)
+            for sk in (3, 5, 6):
+                add({"ntok": 192, "split": sk})
+            continue
         for sk in (0, 1, 3, 4):
             if (sk == 3 and nt != 256) or (sk == 4 and nt > 32 and nt != 128):
                 continue

@@ -282,12 +282,14 @@ def test_gemm_all_tile_plans(ntok, split):
 
 
 @pytest.mark.parametrize("scheme,gs", [("per-channel", 0), ("per-group", 128), ("per-group", 32)])
-def test_gemm_pair_tiles(scheme, gs):
-    """2-CTA pair plans (tcgen05.mma.cta_group::2, 256-channel x 256-token tiles):
-    whole tiles, stream-K and hybrid; odd channel-tile counts, ragged tokens,
-    partial last k-block, few pairs."""
+@pytest.mark.parametrize("ntok", [256, 192])
+def test_gemm_pair_tiles(scheme, gs, ntok):
+    """2-CTA pair plans (tcgen05.mma.cta_group::2, 256-channel x 256- or
+    192-token tiles; the 192-token tile double-buffers its accumulators): whole
+    tiles, stream-K and hybrid; odd channel-tile counts, ragged tokens, partial
+    last k-block, few pairs, several tiles per pair."""
     for (m, k, n, grid) in ((77, 2304, 640, 0), (256, 1024, 384, 0), (300, 896, 1024, 0), (600, 1152, 1000, 7),
-                            (1, 256, 128, 0), (513, 4096, 256, 4)):
+                            (1, 256, 128, 0), (513, 4096, 256, 4), (1024, 1024, 1280, 4)):
         x16, qw_o = _rand_problem(m, k, n, scheme, gs or 128, seed=m + n)
         aq_o = O.quant_act_per_token(x16.astype(np.float64))
         run_o = O.w4a8_gemm_per_channel if scheme == "per-channel" else O.w4a8_gemm_per_group
@@ -298,9 +300,9 @@ def test_gemm_pair_tiles(scheme, gs):
         # 3 = whole pair tiles, 5 = stream-K over pair units, 6 = whole-tile waves + stream-K remainder
         for split in (3, 5, 6):
             for _ in range(2):  # the split plans must leave the workspace zeroed for the next launch
-                out = Q.gemm.run_gemm(aq, prep, n, True, cfg={"ntok": 256, "split": split, "grid": grid})
-                assert same_bits(out.acc, want.acc), (scheme, gs, m, k, n, grid, split)
-                assert same_bits(out.y, want.y), (scheme, gs, m, k, n, grid, split)
+                out = Q.gemm.run_gemm(aq, prep, n, True, cfg={"ntok": ntok, "split": split, "grid": grid})
+                assert same_bits(out.acc, want.acc), (scheme, gs, ntok, m, k, n, grid, split)
+                assert same_bits(out.y, want.y), (scheme, gs, ntok, m, k, n, grid, split)
 
 
 @pytest.mark.parametrize("scheme,gs", [("per-channel", 0), ("per-group", 128), ("per-group", 32)])
