@@ -1708,11 +1708,14 @@ static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
   const double mt = (double)std::min<int64_t>(lp.ntok, M) / 16.0;
   const double epi = kE0 + kE1 * mt;
   if (lp.csplit > 1 && lp.ntok == 128) {
-    // big-CTA cluster split-K: the per-CTA k-blocks at the 1-CTA/SM pace plus the
-    // DSMEM exchange ((S-1)/S x 64 KiB at ~15 B/clk) and the epilogue
+    // big-CTA cluster split-K: linear fit (0.3 us rms, 0.6 us max) to 14 measured
+    // points on 4096x4096 / 11008x4096, M = 32..256, S = 2 / 4 (graph-timed, cold
+    // weights): per-CTA k-blocks, the DSMEM exchange share (S-1)/S, the valid
+    // 16-token chunks, and a second token tile
     const double ucta_cs = (double)((lp.kb_per_tile + lp.csplit - 1) / lp.csplit);
-    const double xchg = (lp.csplit - 1.0) / lp.csplit * 65536.0 / 15.0 / clk;
-    return T0 + ucta_cs * u + xchg + epi;
+    const double mtc = (double)std::min<int64_t>(M, 128) / 16.0;
+    return -0.173 + 0.558 * ucta_cs + 7.826 * (lp.csplit - 1.0) / lp.csplit + 0.225 * mtc +
+           (lp.tok_tiles > 1 ? 1.386 : 0.0);
   }
   if (lp.csplit > 1) {
     // cluster split-K (linear fit to profiles/r01_csplit_sweep.jsonl, 7% rms): a
@@ -1748,7 +1751,9 @@ static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force
   // CTA it only fits 2 weight + 2 activation stages, and the NTOK=128 plan
   // measured faster at every M it would cover (r01_tileplan_sweep_v2)
   for (int nt : {16, 32, 128, 192, 256}) {
-    if (nt > 32 && nt / 4 >= M) break;  // a smaller tile already covers every token
+    // a smaller tile already covers every token (but the 128-token cluster plan
+    // spreads a few channel tiles over more SMs from M = 17 on)
+    if (nt > 32 && nt / 4 >= M && !(nt == 128 && M > 16)) break;
     if (nt == 192) {
       // 192-token pair tiles (double-buffered accumulators) stay a forced-plan option:
       // measured slower than the 256-token pair tile wherever it would be picked
@@ -1769,6 +1774,7 @@ static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force
       if (sk == 2 || (sk == 3 && (nt != 256 || mode == kModeI8)) ||
           (sk == 4 && ((nt > 32 && nt != 128) || mode == kModeI8)))
         continue;
+      if (nt == 128 && nt / 4 >= M && sk != 4) continue;  // (only the cluster plan at M <= 32)
       const LaunchPlan lp = plan_for(mode, M, N, K, nt, sk, 0);
       if (lp.tiles > 65536) continue;
       const double t = plan_cost_us(lp, M);
