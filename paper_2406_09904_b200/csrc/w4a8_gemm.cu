@@ -121,13 +121,13 @@ struct Cfg {
   static constexpr int kConvWarp0 = 0;
   static constexpr int kEpiWarp0 = kNumConvWarps;
   // big CTA: TMEM allocator, activation producer, weight producer and MMA warps;
-  // small CTA: the MMA warp allocates TMEM. Weights and activations have their
-  // own producer warps in both: the weight ring keeps streaming (and the
-  // converters keep filling TMEM A buffers) while the activation producer sits
-  // in the PDL wait, so a decode CTA has all the k-blocks the rings hold
-  // loaded, and kABufs of them converted, before the previous kernel finishes.
+  // small CTA: the MMA warp allocates TMEM, and ONE producer warp runs both
+  // rings in k-block order (weights kWStages ahead, issued before the CTA
+  // set-up barrier). A separate weight producer that keeps streaming through
+  // the PDL wait (QQQ_SMALL_TWO_PRODUCERS, 15 warps at 64 registers) measured
+  // 7% slower on 4096x4096 decode chains and equal elsewhere.
   static constexpr int kAllocWarp = kEpiWarp0 + kNumEpiWarps;
-#ifdef QQQ_SMALL_ONE_PRODUCER
+#ifndef QQQ_SMALL_TWO_PRODUCERS
   static constexpr int kActProducerWarp = kAllocWarp + 1;
   static constexpr int kWProducerWarp = kSmall ? kAllocWarp + 1 : kAllocWarp + 2;
 #else
@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
   // then warp-uniform and live in uniform registers. Issuing tcgen05.mma from
   // a divergent single lane costs ~150 cycles per MMA (R2UR waterfall,
   // scripts/mma_probe.cu) against a 16-cycle issue floor at N = 16.
-#ifdef QQQ_SMALL_ONE_PRODUCER
+#ifndef QQQ_SMALL_TWO_PRODUCERS
   if (C::kSmall && warp == C::kWProducerWarp) {
     // ========== producer warp (small CTA): weight + activation rings ==========
     // One in-order loop over this CTA's k-blocks i = 0..total-1: the weight
@@ -1575,9 +1575,11 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
     // 32-token clusters are kept to one CTA per SM: with two co-resident 32-token
     // cluster CTAs per SM, stress runs (scripts/stress_plans.py, 800 launches)
     // saw one TMEM lane quadrant of one CTA's partial corrupted in 1-10% of the
-    // launches (never with one CTA per SM, never with 16-token clusters).
+    // launches (never with one CTA per SM, never with 16-token clusters; not
+    // from the TMEM column budget either: with 64 spare columns per CTA it persists).
+    static const bool allow32 = getenv("QQQ_EXP_NTOK32_TWO_PER_SM") != nullptr;  // developer A/B switch
     const int slots = (force_grid > 0 ? std::min(force_grid, num_sms()) : num_sms()) *
-                      (ntok == 32 ? 1 : ctas_per_sm(mode, ntok));
+                      ((ntok == 32 && !allow32) ? 1 : ctas_per_sm(mode, ntok));
     // Cluster size S <= 8 (portable), receive buffer [S][ceil(128/S)][NTOK] int32
     // within the 16 KiB partial ring (every S for NTOK=16, divisors of 128 for
     // 32). Measured (profiles/r01_csplit_size_sweep.txt): the fastest S is the

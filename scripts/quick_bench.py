@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--cfgs", default="auto", help="';'-separated JSON tile plans or 'auto'")
     ap.add_argument("--fp16", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few plain launches (for ncu), no timing")
+    ap.add_argument("--reps", type=int, default=0, help="cold replicas per point (default: > 2.5x L2)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     cfgs = [None if c == "auto" else json.loads(c) for c in a.cfgs.split(";")]
@@ -31,7 +32,7 @@ def main():
         k, n = map(int, shp.split("x"))
         for scheme in a.schemes.split(","):
             qw, fused, prep = B.make_weights(k, n, scheme, 0, dev)
-            R = max(2, math.ceil(2.5 * B.L2_BYTES / (k * n / 2)))
+            R = a.reps or max(2, math.ceil(2.5 * B.L2_BYTES / (k * n / 2)))
             if a.profile:
                 R = 2
             reps = [prep] + [G.PreparedWeights(prep.mode, prep.w.clone(), None if prep.sc is None else prep.sc.clone(),
