@@ -1,3 +1,3 @@
-timeout 900 python -m pytest tests/test_pipeline.py tests/test_gpu_parity.py -q -p no:cacheprovider -k "smooth or pipeline or quant or apply" > gpurun_out/pytest_q.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_q.log
-tail -3 gpurun_out/pytest_q.log; grep -m5 "Error\|assert" gpurun_out/pytest_q.log
-timeout 600 python scripts/c4_probe.py > gpurun_out/c4_probe.txt 2>&1; cat gpurun_out/c4_probe.txt
+QQQ_LIB_PATH=paper_2406_09904_b200/lib/lsu.so timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider -k "gemm" > gpurun_out/pytest_q.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_q.log
+tail -2 gpurun_out/pytest_q.log; grep -m3 "Error" gpurun_out/pytest_q.log
+LIBS="prod lsu prod lsu" QB="--shapes 4096x4096,4096x11008,11008x4096 --ms 1,16,32" bash scripts/gpu_abq.sh
