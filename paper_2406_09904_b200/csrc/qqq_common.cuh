@@ -12,6 +12,15 @@
 
 #define QQQ_DEVICE __device__ __forceinline__
 
+// Watchdog of the spin waits (ns): a wait that never completes traps the launch
+// instead of hanging the GPU. Sanitizer builds raise it (tools serialise CTAs).
+#ifndef QQQ_WATCHDOG_NS
+#define QQQ_WATCHDOG_NS 4000000000ull
+#endif
+#ifndef QQQ_WATCHDOG_ITERS
+#define QQQ_WATCHDOG_ITERS (1u << 24)
+#endif
+
 namespace qqq {
 
 // ----------------------------------------------------------------------------
@@ -101,7 +110,7 @@ QQQ_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     if (done) return;
 #ifndef QQQ_NO_WATCHDOG
-    if (n > (1u << 24)) __trap();
+    if (n > QQQ_WATCHDOG_ITERS) __trap();
 #endif
   }
 }
@@ -130,7 +139,7 @@ QQQ_DEVICE void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t0 == 0) t0 = t;
-      else if (t - t0 > 4000000000ull) __trap();
+      else if (t - t0 > QQQ_WATCHDOG_NS) __trap();
     }
 #endif
   }
@@ -182,7 +191,7 @@ QQQ_DEVICE void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t0 == 0) t0 = t;
-      else if (t - t0 > 4000000000ull) __trap();
+      else if (t - t0 > QQQ_WATCHDOG_NS) __trap();
     }
 #endif
   }
@@ -207,7 +216,7 @@ QQQ_DEVICE void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t0 == 0) t0 = t;
-      else if (t - t0 > 4000000000ull) __trap();
+      else if (t - t0 > QQQ_WATCHDOG_NS) __trap();
     }
 #endif
   }
@@ -241,7 +250,7 @@ QQQ_DEVICE void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
     __nanosleep(ns);
     ns = ns < 256 ? ns * 2 : 256;
 #ifndef QQQ_NO_WATCHDOG
-    if (n > (1u << 24)) __trap();
+    if (n > QQQ_WATCHDOG_ITERS) __trap();
 #endif
   }
 }

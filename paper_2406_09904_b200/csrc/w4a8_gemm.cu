@@ -844,9 +844,11 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             // whole warp, so lane 0's data dependency covers every lane).
             // (Per-lane arrives with a 32x arrival count were measured to complete
             // the phase early — stages refilled under the readers — so the
-            // warp-level release stays; compute-sanitizer racecheck reports this
-            // lane-0-after-__syncwarp release as a WAR hazard on lanes 1..31.)
-            __syncwarp();
+            // warp-level release stays.)
+            // a per-warp named barrier (ids 8-15) rather than __syncwarp: the same
+            // ordering, in a form compute-sanitizer racecheck follows (measured
+            // perf-neutral)
+            named_bar_sync(8 + (warp & 7), 32);
             if (lane == 0) mbar_arrive_addr(smem_u32(&w_empty[ws]) + dep);
           }
           if (++ws == C::kWStages) {
@@ -1317,7 +1319,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
                 const unsigned long long t = gtimer();
                 if (t0 == 0)
                   t0 = t;
-                else if (t - t0 > 4000000000ull)
+                else if (t - t0 > QQQ_WATCHDOG_NS)
                   __trap();
               }
 #endif

@@ -1,1 +1,3 @@
-timeout 1500 python scripts/quick_bench.py --shapes 4096x4096,4096x11008,11008x4096,8192x8192,8192x28672,28672x8192 --ms 256,512,1024 --cfgs 'auto;{"ntok":256,"split":3};{"ntok":256,"split":1};{"ntok":256,"split":0};{"ntok":192,"split":3};{"ntok":192,"split":5};{"ntok":128,"split":0};{"ntok":128,"split":1}' > gpurun_out/qb_prefill.txt 2>&1
+QQQ_LIB_PATH=paper_2406_09904_b200/lib/nbar.so timeout 600 compute-sanitizer --tool racecheck --racecheck-report all --print-limit 10 python scripts/sanitize_cases.py --quick > gpurun_out/racecheck_nbar.txt 2>&1; echo "exit $?" >> gpurun_out/racecheck_nbar.txt
+grep -v "^=========     \|Host Frame\|^========= $" gpurun_out/racecheck_nbar.txt | tail -14
+LIBS="prod nbar" QB="--shapes 4096x4096,4096x11008 --ms 1,16,128,1024" bash scripts/gpu_abq.sh
