@@ -166,13 +166,15 @@ int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const int
 /* Generic form (mode PC/PG/I8) with an optional tile-plan override; I8 with
  * s_col == NULL is gemm_i8_i32 (gemm.py:145-154, acc only). */
 typedef struct qqq_gemm_config {
-  int ntok;  /* tokens per UMMA tile: 16/32/64/128/256, 0 = auto */
+  int ntok;  /* tokens per UMMA tile: 16/32/64/128/192/256, 0 = auto (192: pair plans only) */
   int grid;  /* CTAs for stream-K, 0 = auto */
   int split; /* -1 auto, 0 whole tiles, 1 stream-K, 2 whole-tile waves + stream-K remainder,
-              * 3 whole 256x256 pair tiles (2-CTA clusters, ntok 256), 4 cluster split-K
-              * (ntok 16/32: one tile per cluster, DSMEM reduction), 5 stream-K over pair
-              * tiles, 6 pair-tile waves + stream-K remainder */
-  int csplit; /* split 4 only: cluster size S in 2..8 (0 = the planner's choice) */
+              * 3 whole 256-channel pair tiles (2-CTA clusters, ntok 256 or 192), 4 cluster
+              * split-K (one tile per cluster, DSMEM reduction: ntok 16/32 half-SM CTAs,
+              * reduce-scatter by channel rows; ntok 128 whole-SM CTAs, by token range),
+              * 5 stream-K over pair tiles, 6 pair-tile waves + stream-K remainder */
+  int csplit; /* split 4 only: cluster size S (2..8 for ntok 16/32, 2 or 4 for ntok 128;
+               * 0 = the planner's choice) */
   void* dbg; /* optional device buffer [grid][64] u64: per-CTA %globaltimer timeline (diagnostics) */
 } qqq_gemm_config;
 
