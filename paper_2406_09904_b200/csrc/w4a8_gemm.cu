@@ -1766,9 +1766,17 @@ static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force
       // (4096x11008 M=1024 54.3 vs 51.8 us, 11008x4096 66.3 vs 38.3 us): prefill is
       // co-bound by the INT4->INT8 conversion, which a 192-token tile repeats for
       // 6 instead of 4 token tiles at M = 1024, more than the hidden epilogue saves.
-      if (mode == kModeI8 || !getenv("QQQ_EXP_AUTO_192")) continue;
+      // One regime where it measured faster: two 256-token tiles per channel pair
+      // would fill between one and 1.6 waves of CTA pairs (4096x11008 M=512: 30.6
+      // vs 33.8 us); three 192-token tiles fill the pairs more evenly and hide their
+      // epilogues.
+      if (mode == kModeI8) continue;
+      const LaunchPlan lp256 = plan_for(mode, M, N, K, 256, 3, 0);
+      const double waves256 = (double)lp256.tiles / std::max(1, pair_slots(mode));
+      const bool regime = M > 448 && M <= 576 && waves256 > 1.0 && waves256 < 1.6;
+      if (!regime && !getenv("QQQ_EXP_AUTO_192")) continue;
       const LaunchPlan lp = plan_for(mode, M, N, K, nt, 3, 0);
-      const double t = plan_cost_us(lp, M);
+      const double t = regime ? 0.0 : plan_cost_us(lp, M);
       if (lp.tiles <= 65536 && t < best_t) {
         best_t = t;
         best = lp;
