@@ -29,6 +29,7 @@
 //   * Epilogue: f64 (acc * s_a) * s_col then cvt.rn.f16.f64 -> bit-identical
 //     to the reference's f64 epilogue with a single final rounding.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -89,6 +90,11 @@ struct Cfg {
   // tile is otherwise starved of activation + weight bytes in flight.
   static constexpr bool kPair = PAIR;
   static constexpr int kTokLoad = PAIR ? NTOK / 2 : NTOK;  // activation rows this CTA loads per k-block
+  // 384-token pair tiles: two MMAs of N = 192 per K step (UMMA N <= 256). Each CTA
+  // loads two 96-row chunks, tokens [96r, 96r+96) and [192+96r, 192+96r+96) of the
+  // tile, so accumulator column c is token c for both MMAs.
+  static constexpr int kMmaSplit = NTOK > 256 ? 2 : 1;
+  static constexpr int kMmaN = NTOK / kMmaSplit;
   // ---- CTA shape. Decode/mid tiles (NTOK <= 64) use a half-SM CTA: two per SM,
   // so a CTA's prologue / first-byte latency / epilogue tail overlaps the other
   // CTA's stream, and under PDL the next kernel's CTAs start (and prefetch
@@ -156,7 +162,7 @@ struct Cfg {
   // the 1 B/weight operand off the shared-memory crossbar, which otherwise
   // bounds the decode stream (TMA write + STS + MMA read of every weight).
   static constexpr int kACols = BK / 4;
-  static constexpr int kAccBufs = NTOK == 256 ? 1 : 2;
+  static constexpr int kAccBufs = NTOK >= 256 ? 1 : 2;
   static constexpr int kAccCols = kAccBufs * NTOK;
   static constexpr int kABufsMax = kConvert ? (kTmemBudget - kAccCols) / kACols : 8;
   static constexpr int kRingBudget = kSmemBudget - 2048 - NTOK * 12 - kEpiSmem;
@@ -199,8 +205,8 @@ struct Cfg {
   // per-group: the converter emits w8 + 128 (no XOR); the MMA runs u8 x s8 and
   // the epilogue subtracts 128 * rowsum(a) — exact in int32 (K <= 65536)
   static constexpr bool kU8 = MODE == kModePG;
-  static constexpr uint32_t kIdesc = make_idesc_i8(PAIR ? 256 : 128, NTOK, kU8);
-  static_assert(NTOK % 16 == 0 && NTOK >= 16 && NTOK <= 256, "invalid UMMA N");
+  static constexpr uint32_t kIdesc = make_idesc_i8(PAIR ? 256 : 128, kMmaN, kU8);
+  static_assert(kMmaN % 16 == 0 && kMmaN >= 16 && kMmaN <= 256 && (kMmaSplit == 1 || PAIR), "invalid UMMA N");
   static_assert(BK % 128 == 0, "BK must be a multiple of the 128-byte swizzle atom");
 };
 
@@ -665,8 +671,16 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           if constexpr (PAIR) {
             // each CTA loads its half of the tokens; the bytes of both count on the even CTA's barrier
             if (crank == 0) mbar_arrive_expect_tx(&kb_full[s], 2 * C::kXBytes);
-            tma_load_3d_pair(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0 + (int)crank * C::kTokLoad,
-                             kb * (BK / 128), kb_full_cl + s * 8);
+            if constexpr (C::kMmaSplit == 2) {
+              constexpr int kHalf = C::kTokLoad / 2;  // 96 rows per chunk
+              tma_load_3d_pair(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0 + (int)crank * kHalf,
+                               kb * (BK / 128), kb_full_cl + s * 8);
+              tma_load_3d_pair(smem + C::kOffX + s * C::kXBytes + kHalf * 128, &act_map, 0,
+                               tok0 + NTOK / 2 + (int)crank * kHalf, kb * (BK / 128), kb_full_cl + s * 8);
+            } else {
+              tma_load_3d_pair(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0 + (int)crank * C::kTokLoad,
+                               kb * (BK / 128), kb_full_cl + s * 8);
+            }
           } else {
 #ifdef QQQ_EXP_HALF_X
             mbar_arrive_expect_tx(&kb_full[s], NTOK >= 128 ? C::kXBytes / 2 : C::kXBytes);
@@ -717,7 +731,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             // B: SWIZZLE_128B [k-atom][NTOK rows][128 B]; 32 B K-steps inside the atom
             const uint64_t b_desc = b_desc0 + (uint64_t)(((kk / 4) * (C::kTokLoad * 128) + (kk % 4) * 32) >> 4);
             const uint32_t acc = kk > 0 ? 1u : acc0;
-            if constexpr (PAIR) {
+            if constexpr (PAIR && C::kMmaSplit == 2) {
+              static_assert(BK == 128, "384-token tiles: one 128-byte swizzle atom per k-block");
+              mma_i8_ts_pair(d_tmem, a_tmem + kk * 8, b_desc, C::kIdesc, acc);
+              mma_i8_ts_pair(d_tmem + C::kMmaN, a_tmem + kk * 8, b_desc + (uint64_t)((C::kTokLoad / 2 * 128) >> 4),
+                             C::kIdesc, acc);
+            } else if constexpr (PAIR) {
               mma_i8_ts_pair(d_tmem, a_tmem + kk * 8, b_desc, C::kIdesc, acc);
             } else if constexpr (C::kConvert) {
               mma_i8_ts(d_tmem, a_tmem + kk * 8, b_desc, C::kIdesc, acc);  // A: 8 TMEM columns per K=32
@@ -1608,7 +1627,10 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
     return lp;
   }
   const bool pair_plan = split == 3 || split == 5 || split == 6;
-  if (pair_plan && ((ntok != 256 && ntok != 192) || mode == kModeI8)) split = split == 3 ? 0 : split == 5 ? 1 : 2;
+  if (pair_plan && ((ntok != 256 && ntok != 192 && ntok != 384) || mode == kModeI8))
+    split = split == 3 ? 0 : split == 5 ? 1 : 2;
+  if (ntok == 384 && (split == 0 || split == 1 || split == 2 || split == 5 || split == 6))
+    split = 3;  // (384-token tiles: whole pair tiles only)
   if (split == 3 || split == 5 || split == 6) {
     // pair tiles: 3 = whole pair tiles, 5 = stream-K over (pair tile, k-block) units
     // across the CTA pairs, 6 = whole-tile waves + the remainder stream-K'd
@@ -1798,6 +1820,18 @@ static LaunchPlan make_plan(int mode, int64_t M, int64_t N, int64_t K, int force
       }
     }
   }
+  // 384-token pair tiles (two N=192 MMAs per K step, each weight tile converted
+  // for 384 tokens): taken over the 256-token pair tile when they need fewer
+  // waves of CTA pairs after a 15% longer tile (measured: 8192x8192 M=768 51.0 ->
+  // 40.7 us, 28672x8192 M=768 165 -> 121, 4096x11008 M=1024 52.1 -> 46.9,
+  // 8192x28672 M=1024 222 -> 196; slower wherever the wave count does not drop)
+  if (best.ntok == 256 && M >= 640 && mode != kModeI8) {
+    const LaunchPlan lp256 = plan_for(mode, M, N, K, 256, 3, 0);
+    const LaunchPlan lp384 = plan_for(mode, M, N, K, 384, 3, 0);
+    const double pairs = std::max(1, pair_slots(mode));
+    const double w256 = std::ceil(lp256.tiles / pairs), w384 = std::ceil(lp384.tiles / pairs);
+    if (lp384.pair && w384 * 1.15 < w256) best = lp384;
+  }
   return best;
 }
 
@@ -1866,6 +1900,8 @@ static int launch_pair(int ntok, const CUtensorMap& map, const CUtensorMap& ymap
     return kErrConfig;
   else if (ntok == 192)  // double-buffered accumulators (2 x 192 + 4 A buffers of 32 TMEM columns)
     return launch_t<MODE, 192, kPairBk, true>(map, ymap, p, grid, st);
+  else if (ntok == 384)  // 384-token tiles: each weight tile converted for more tokens
+    return launch_t<MODE, 384, kPairBk, true>(map, ymap, p, grid, st);
   else
     return launch_t<MODE, 256, kPairBk, true>(map, ymap, p, grid, st);
 }
@@ -1943,7 +1979,9 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
 #ifdef QQQ_EXP_HALF_X
   cuuint32_t box[3] = {128u, (cuuint32_t)(lp.ntok >= 128 ? lp.ntok / 2 : lp.ntok), (cuuint32_t)(lp.bk / 128)};
 #else
-  cuuint32_t box[3] = {128u, (cuuint32_t)(lp.pair ? lp.ntok / 2 : lp.ntok), (cuuint32_t)(lp.bk / 128)};
+  // (pair CTAs load half the tile's tokens; 384-token tiles in two 96-row chunks)
+  cuuint32_t box[3] = {128u, (cuuint32_t)(lp.ntok == 384 ? 96 : lp.pair ? lp.ntok / 2 : lp.ntok),
+                       (cuuint32_t)(lp.bk / 128)};
 #endif
   cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)aq, dims, strides, box, estr,

@@ -119,6 +119,8 @@ def candidate_plans(mode, m, n, k):
             for sk in (3, 5, 6):
                 add({"ntok": 192, "split": sk})
             continue
+    if m > 96:  # 384-token pair tiles (whole tiles only)
+        add({"ntok": 384, "split": 3})
         for sk in (0, 1, 3, 4):
             if (sk == 3 and nt != 256) or (sk == 4 and nt > 32 and nt != 128):
                 continue

@@ -282,10 +282,11 @@ def test_gemm_all_tile_plans(ntok, split):
 
 
 @pytest.mark.parametrize("scheme,gs", [("per-channel", 0), ("per-group", 128), ("per-group", 32)])
-@pytest.mark.parametrize("ntok", [256, 192])
+@pytest.mark.parametrize("ntok", [256, 192, 384])
 def test_gemm_pair_tiles(scheme, gs, ntok):
-    """2-CTA pair plans (tcgen05.mma.cta_group::2, 256-channel x 256- or
-    192-token tiles; the 192-token tile double-buffers its accumulators): whole
+    """2-CTA pair plans (tcgen05.mma.cta_group::2, 256-channel x 256-, 192- or
+    384-token tiles; the 192-token tile double-buffers its accumulators, the
+    384-token tile issues two N=192 MMAs per K step; whole tiles only): whole
     tiles, stream-K and hybrid; odd channel-tile counts, ragged tokens, partial
     last k-block, few pairs, several tiles per pair."""
     for (m, k, n, grid) in ((77, 2304, 640, 0), (256, 1024, 384, 0), (300, 896, 1024, 0), (600, 1152, 1000, 7),
