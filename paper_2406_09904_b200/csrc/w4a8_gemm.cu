@@ -116,7 +116,10 @@ struct Cfg {
   // covering all 128 rows and BK of k) takes the k-blocks it with it % groups ==
   // g, so each warp's fixed per-k-block latency (barrier waits, TMEM store
   // completion, arrive) overlaps the other group's k-block
-  static constexpr int kConvGroups = PAIR ? QQQ_PAIR_CONV_GROUPS : 1;
+#ifndef QQQ_BIG_CONV_GROUPS
+#define QQQ_BIG_CONV_GROUPS 1
+#endif
+  static constexpr int kConvGroups = PAIR ? QQQ_PAIR_CONV_GROUPS : kSmall ? 1 : QQQ_BIG_CONV_GROUPS;
   static constexpr int kConvPerGroup = kNumConvWarps / kConvGroups;
   static_assert(kConvPerGroup % 4 == 0, "a converter group covers the 4 TMEM lane quadrants");
 #ifndef QQQ_BIG_EPI_WARPS
@@ -146,7 +149,10 @@ struct Cfg {
   static constexpr int kTmemBudget = kSmall ? 256 : 512;
   // split-K partial ring depth per epilogue group (2 when the shared memory allows)
   // (the NTOK=256 prefill tiles, mostly whole tiles, give it up for activation stages)
-  static constexpr int kPartBufs = (kEpiGroups > 2 && NTOK >= 256) ? 1 : 2;  // (part_full holds 2 per group)
+#ifndef QQQ_BIG_PARTBUFS
+#define QQQ_BIG_PARTBUFS 2
+#endif
+  static constexpr int kPartBufs = (kEpiGroups > 2 && NTOK >= 256) ? 1 : kSmall ? 2 : QQQ_BIG_PARTBUFS;  // (part_full holds 2 per group)
   static constexpr int kEpiSmem = kNumEpiWarps * 2048 + kEpiGroups * kPartBufs * 8192;  // y staging + partial ring
   // Two rings. Weights: their own TMA ring (released by the converters once
   // the packed bytes are consumed, or by the MMA in I8 mode). K-blocks: ring
@@ -178,7 +184,10 @@ struct Cfg {
 #ifndef QQQ_SMALL_XCAP
 #define QQQ_SMALL_XCAP 4
 #endif
-  static constexpr int kXCapWanted = PAIR ? QQQ_PAIR_XCAP : kSmall ? QQQ_SMALL_XCAP : 4;
+#ifndef QQQ_BIG_XCAP
+#define QQQ_BIG_XCAP 4
+#endif
+  static constexpr int kXCapWanted = PAIR ? QQQ_PAIR_XCAP : kSmall ? QQQ_SMALL_XCAP : QQQ_BIG_XCAP;
   static constexpr int kXCap = kABufsMax < kXCapWanted ? kABufsMax : kXCapWanted;
   static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > kXCap ? kXCap : kXStagesRaw);
   static constexpr int kABufs = kConvert ? kXStages : 0;
@@ -231,6 +240,18 @@ QQQ_DEVICE unsigned long long gtimer() {
   } while (0)
 #endif
 
+// whole-SM weight producer: spins (a suspended try_wait woke measurably late
+// behind the converters' release; 1-2% at mid/prefill M)
+#ifndef QQQ_WPROD_SLEEP
+#define wprod_wait mbar_wait
+#else
+#define wprod_wait mbar_wait_sleep
+#endif
+#ifdef QQQ_XPROD_SPIN
+#define xprod_wait mbar_wait
+#else
+#define xprod_wait mbar_wait_sleep
+#endif
 #ifdef QQQ_CONV_SLEEP
 #define conv_wait mbar_wait_sleep
 #else
@@ -314,6 +335,26 @@ QQQ_DEVICE void dequant16(const uint32_t (&r)[16], const double* sa, double s_co
   }
 }
 
+// The same for all 16 tokens, unpredicated (TMA-stored chunks: rows past M
+// are clipped by the store, so their values are never written). Phases of 8
+// independent conversions / products: the predicated per-token form compiled
+// to one dependent DADD -> DMUL -> DMUL -> F2F chain after another and ran at
+// half the FP64 pipe's rate (scripts/epi_probe.cu: 10 values/clk/SM).
+QQQ_DEVICE void dequant16_all(const uint32_t (&r)[16], const double* sa, double s_col, uint16_t (&h)[16]) {
+#pragma unroll
+  for (int g = 0; g < 16; g += 8) {
+    double d[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] = i32_to_f64_exact((int32_t)r[g + i]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] *= sa[g + i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] *= s_col;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[g + i] = __half_as_ushort(f64_to_f16_rn(d[i]));
+  }
+}
+
 // Dequant epilogue for up to 16 consecutive tokens of one output channel n:
 // y = f16((acc * s_a[t]) * s_col[n]) in f64 with one final RN rounding
 // (gemm.py:182-184 / 200-202); acc written as-is when requested.
@@ -329,7 +370,7 @@ QQQ_DEVICE void store_outputs(const GemmParams& p, const uint32_t (&r)[16], cons
   }
   if (p.s_col && !p.y_tma) {
     uint16_t h[16];
-    dequant16(r, sa, s_col, h);
+    dequant16_all(r, sa, s_col, h);  // (entries past nvalid are computed but not stored)
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (i < nvalid) reinterpret_cast<uint16_t*>(p.y)[(int64_t)(t0 + i) * p.ldy + n] = h[i];
@@ -635,13 +676,14 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
 #pragma unroll 1
       for (int kb = kb0; kb < kb1; ++kb, ++i) {
         if (i >= pre) {
-          mbar_wait_sleep(&w_empty[s], ph ^ 1);
+          wprod_wait(&w_empty[s], ph ^ 1);
           if (elect_one()) {
             // the last k-block of a tile may hold fewer super-slabs (K_pad % BK != 0):
             // the stale rest of the stage meets zero-filled (OOB) activations
             const int nss = min(BK / 128, p.ss_per_tile - kb * (BK / 128));
             const uint32_t wbytes = (uint32_t)(nss * p.ss_bytes);
             mbar_arrive_expect_tx(&w_full[s], wbytes);
+            if (i < 16) QQQ_STAMP(155 + i);
             const int64_t ss0 = (int64_t)n_tile * p.ss_per_tile + (int64_t)kb * (BK / 128);
             bulk_g2s(smem + C::kOffW + s * C::kWBytes, p.w + ss0 * p.ss_bytes, wbytes, &w_full[s]);
           }
@@ -665,7 +707,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       const int tok0 = (tile % p.tok_tiles) * NTOK;
 #pragma unroll 1
       for (int kb = kb0; kb < kb1; ++kb, ++xit) {
-        mbar_wait_sleep(&kb_empty[s], ph ^ 1);
+        xprod_wait(&kb_empty[s], ph ^ 1);
         if (lane == 0 && xit < 16) QQQ_STAMP(112 + xit);
         if (elect_one()) {
           if constexpr (PAIR) {
@@ -1247,7 +1289,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             if (p.y_tma) {
               uint16_t* stg = reinterpret_cast<uint16_t*>(ystage) + (ych & 1) * 512;
               uint16_t h[16];
-              dequant16(r, sa_smem + c0, s_col, h, tvalid - c0);
+              dequant16_all(r, sa_smem + c0, s_col, h);
               if (lane == 0) bulk_wait_read<1>();
               __syncwarp();
 #pragma unroll
@@ -1389,17 +1431,21 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             // (OOB rows/cols clipped): no cross-warp barrier on the store path
             uint16_t* stg = reinterpret_cast<uint16_t*>(ystage) + (ych & 1) * 512;
             uint16_t h[16];
-            dequant16(r, sa_smem + c0, s_col, h, tvalid - c0);
+            dequant16_all(r, sa_smem + c0, s_col, h);
+            if (lead && seg == 0 && li < 4) QQQ_STAMP(128 + li);
             if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer two chunks ago has read it
             __syncwarp();
+            if (lead && seg == 0 && li < 4) QQQ_STAMP(132 + li);
 #pragma unroll
             for (int i = 0; i < 16; ++i) stg[i * 32 + lane] = h[i];
             fence_proxy_async_smem();
             __syncwarp();
+            if (lead && seg == 0 && li < 4) QQQ_STAMP(136 + li);
             if (lane == 0) {
               tma_store_2d(&y_map, stg, n_tile * 128 + q * 32, tok0 + c0);
               bulk_commit();
             }
+            if (lead && seg == 0 && li < 4) QQQ_STAMP(140 + li);
             ++ych;
           }
         }
@@ -1627,7 +1673,7 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
     return lp;
   }
   const bool pair_plan = split == 3 || split == 5 || split == 6;
-  if (pair_plan && ((ntok != 256 && ntok != 192 && ntok != 384) || mode == kModeI8))
+  if (pair_plan && ((ntok != 256 && ntok != 192 && ntok != 384 && ntok != 128) || mode == kModeI8))
     split = split == 3 ? 0 : split == 5 ? 1 : 2;
   if (ntok == 384 && (split == 0 || split == 1 || split == 2 || split == 5 || split == 6))
     split = 3;  // (384-token tiles: whole pair tiles only)
@@ -1902,6 +1948,8 @@ static int launch_pair(int ntok, const CUtensorMap& map, const CUtensorMap& ymap
     return launch_t<MODE, 192, kPairBk, true>(map, ymap, p, grid, st);
   else if (ntok == 384)  // 384-token tiles: each weight tile converted for more tokens
     return launch_t<MODE, 384, kPairBk, true>(map, ymap, p, grid, st);
+  else if (ntok == 128)  // 128-token pair tiles: half the activation bytes per SM of a 128-token tile
+    return launch_t<MODE, 128, kPairBk, true>(map, ymap, p, grid, st);
   else
     return launch_t<MODE, 256, kPairBk, true>(map, ymap, p, grid, st);
 }
@@ -1993,7 +2041,8 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   CUtensorMap ymap;
   memset(&ymap, 0, sizeof(ymap));
   int y_tma = 0;
-  if (s_col && y && (ldy * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+  static const bool no_ytma = getenv("QQQ_EXP_NO_YTMA") != nullptr;
+  if (s_col && y && !no_ytma && (ldy * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
     cuuint64_t ydims[2] = {(cuuint64_t)N, (cuuint64_t)M};
     cuuint64_t ystr[1] = {(cuuint64_t)(ldy * 2)};
     cuuint32_t ybox[2] = {32u, 16u};  // one epilogue warp's [16 tok][32 ch] chunk

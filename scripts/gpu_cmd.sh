@@ -1,3 +1,3 @@
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
 tail -2 gpurun_out/pytest_gpu.log; grep FAILED gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python scripts/stress_plans.py > gpurun_out/stress.txt 2>&1; tail -3 gpurun_out/stress.txt

@@ -144,6 +144,7 @@ int main() {
   run<128, true>(d_out);
   run<256, true>(d_out);
   run<256, false>(d_out);
+  run<128, false>(d_out);
   cudaError_t e = cudaDeviceSynchronize();
   printf("err=%s\n", cudaGetErrorString(e));
   return 0;

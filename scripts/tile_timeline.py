@@ -36,8 +36,12 @@ print("CTA exit min/med/max us: %.2f %.2f %.2f" % (ends.min(), np.median(ends), 
 c = d[a.cta]
 f = lambda v: "%.2f" % ((v - t0) / 1e3) if v > 0 else "-"
 print("cta", a.cta, "start", f(c[0]), "exit", f(c[42]))
-print(" kb: full(w) conv_done mma_xfull mma_issued")
+print(" kb: w_issue full(w) | x_issue | conv_done mma_xfull mma_issued")
 for it in range(16):
-    print("  %2d: %s %s %s %s" % (it, f(c[4 + it]), f(c[80 + it]), f(c[96 + it]), f(c[20 + it])))
+    print("  %2d: %s %s | %s | %s %s %s" % (it, f(c[155 + it]), f(c[4 + it]), f(c[112 + it]), f(c[80 + it]), f(c[96 + it]), f(c[20 + it])))
 for sg in range(4):
     print(" seg %d: accfull %s epi_done %s" % (sg, f(c[36 + 2 * sg]), f(c[37 + 2 * sg])))
+print(" epi chunk tmem-ld done (lead warp, seg 0):", " ".join(f(c[44 + li]) for li in range(16)))
+print(" epi loop end %s  stores read %s" % (f(c[154]), f(c[63])))
+for li in range(4):
+    print("  chunk %d: tmem-ld %s dequant %s wait-read %s sts+fence %s store %s" % (li, f(c[44 + li]), f(c[128 + li]), f(c[132 + li]), f(c[136 + li]), f(c[140 + li])))

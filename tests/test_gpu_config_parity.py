@@ -119,10 +119,8 @@ def candidate_plans(mode, m, n, k):
             for sk in (3, 5, 6):
                 add({"ntok": 192, "split": sk})
             continue
-    if m > 96:  # 384-token pair tiles (whole tiles only)
-        add({"ntok": 384, "split": 3})
         for sk in (0, 1, 3, 4):
-            if (sk == 3 and nt != 256) or (sk == 4 and nt > 32 and nt != 128):
+            if (sk == 3 and nt not in (128, 256)) or (sk == 4 and nt > 32 and nt != 128):
                 continue
             if sk == 4:
                 for s in (range(2, 9) if nt <= 32 else (2, 4)):
@@ -132,6 +130,8 @@ def candidate_plans(mode, m, n, k):
         if nt == 256:
             for sk in (5, 6):  # pair stream-K / pair waves + stream-K (forced-plan options)
                 add({"ntok": 256, "split": sk})
+    if m > 96:  # 384-token pair tiles (whole tiles only)
+        add({"ntok": 384, "split": 3})
     return auto, out
 
 

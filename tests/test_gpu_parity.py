@@ -282,7 +282,7 @@ def test_gemm_all_tile_plans(ntok, split):
 
 
 @pytest.mark.parametrize("scheme,gs", [("per-channel", 0), ("per-group", 128), ("per-group", 32)])
-@pytest.mark.parametrize("ntok", [256, 192, 384])
+@pytest.mark.parametrize("ntok", [256, 192, 384, 128])
 def test_gemm_pair_tiles(scheme, gs, ntok):
     """2-CTA pair plans (tcgen05.mma.cta_group::2, 256-channel x 256-, 192- or
     384-token tiles; the 192-token tile double-buffers its accumulators, the
