@@ -184,6 +184,23 @@ int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a,
                      void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
                      const qqq_gemm_config* cfg, qqq_stream_t stream);
 
+/* apply_quant_linear in one launch (replaces pipeline.py:144-152's
+ * `quant_act_per_token(x / s)` + `w4a8_gemm_*` pair; mode PC or PG): the
+ * epilogue warps of the GEMM's first-wave CTAs quantize x / smooth (fp16
+ * [M, K], row pitch ldx; K, ldx multiples of 8, x / smooth / smooth_recip
+ * 16-byte aligned) into q (row pitch ldq as for qqq_w4a8_gemm_ex), s_a and
+ * rowsum -- bit-identical to qqq_act_quant_smooth(_rcp) -- while the weights
+ * stream in; the MMAs start once every row is published. smooth_recip:
+ * qqq_smooth_reciprocal's table or NULL. Non-finite quotients OR
+ * QQQ_STAT_NONFINITE into *status_dev (DataError, quantize.py:85-89). The
+ * workspace is qqq_w4a8_gemm_ex's (its head holds the row counter). */
+int qqq_w4a8_gemm_smooth_fused(int mode, const void* x, int64_t ldx, const double* smooth,
+                               const double* smooth_recip, int8_t* q, int64_t ldq, double* s_a, int32_t* rowsum,
+                               int32_t* status_dev, const void* w_repacked, int64_t group, const double* s_col,
+                               int64_t M, int64_t N, int64_t K, void* y, int64_t ldy, int32_t* acc_opt,
+                               int64_t ldacc, void* workspace, size_t ws_bytes, const qqq_gemm_config* cfg,
+                               qqq_stream_t stream);
+
 /* The tile plan qqq_w4a8_gemm_ex would launch for (mode, M, N, K, cfg): the
  * planner's choice when cfg is NULL or all-auto, else the forced plan as the
  * launch resolves it (out->split is the effective split, out->csplit the

@@ -58,6 +58,8 @@ SIGNATURES = {
     "qqq_w4a8_gemm_pg": (c_int, [P, I64, P, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t, S]),
     "qqq_w4a8_gemm_ex": (c_int, [c_int, P, I64, P, P, P, I64, P, I64, I64, I64, P, I64, P, I64, P, c_size_t,
                                   ctypes.POINTER(GemmConfig), S]),
+    "qqq_w4a8_gemm_smooth_fused": (c_int, [c_int, P, I64, P, P, P, I64, P, P, P, P, I64, P, I64, I64, I64, P, I64,
+                                            P, I64, P, c_size_t, ctypes.POINTER(GemmConfig), S]),
     "qqq_gemm_plan_info": (c_int, [c_int, I64, I64, I64, ctypes.POINTER(GemmConfig), ctypes.POINTER(GemmConfig)]),
     "qqq_test_fused_dequant_quant": (c_int, [P, P, P, I64, c_int, S]),
     "qqq_test_pc_convert": (c_int, [P, P, I64, S]),

@@ -35,6 +35,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "act_quant_dev.cuh"
 #include "qqq_common.cuh"
 #include "qqq_layout.cuh"
 
@@ -77,7 +78,30 @@ struct GemmParams {
   int csplit;               // >1: cluster split-K (decode CTAs): cluster c = tile c, rank r = k-range r of csplit,
                             //     partials reduce-scattered over DSMEM (rank r finalizes channel rows r*128/csplit..)
   unsigned long long* dbg;  // optional per-CTA %globaltimer timeline, diagnostics only
+  // Fused smoothed activation quantization (apply_quant_linear, pipeline.py:144-152), when xsrc
+  // is set: the epilogue warps of CTAs [0, q_ctas) quantize x / smooth (fp16 [M, K], row pitch
+  // ldx) into the activation operand (qdst, row pitch = the TMA map's), s_a and rowsum while the
+  // weights stream in; the activation producers and the epilogue wait for all M rows (a counter
+  // in the workspace head, zero on entry and exit).
+  const __half* xsrc;
+  int64_t ldx;
+  const double* smooth;
+  const double* srecip;  // qqq_smooth_reciprocal table or nullptr (IEEE division)
+  int8_t* qdst;
+  int64_t ldq;
+  double* sa_dst;
+  int32_t* rs_dst;
+  int32_t* status;
+  int q_ctas;
+  // Always 0. A runtime zero the compiler cannot fold: the converters' stage
+  // release is made data-dependent on their shared-memory loads through it
+  // (`dep & zero`); with a literal `and 0` ptxas dropped the dependency.
+  uint32_t zero;
 };
+
+// workspace-head slots of the fused quantization: rows published, CTAs done with them
+constexpr int kQRowsSlot = 65536 - 2;
+constexpr int kQDoneSlot = 65536 - 1;
 
 template <int MODE, int NTOK, int BK, bool PAIR = false>
 struct Cfg {
@@ -353,6 +377,122 @@ QQQ_DEVICE void dequant16_all(const uint32_t (&r)[16], const double* sa, double 
 #pragma unroll
     for (int i = 0; i < 8; ++i) h[g + i] = __half_as_ushort(f64_to_f16_rn(d[i]));
   }
+}
+
+// ---- fused smoothed activation quantization (GemmParams::xsrc) ----
+// The token rows of one epilogue group (128 threads, warps of the group at
+// scratch: 48 bytes): rows blockIdx.x + q_ctas * (grp + ngroups * j). The
+// arithmetic is act_quant_row_kernel<.., kSmooth = true>'s (act_quant.cu):
+// x / s_k by Markstein with the reciprocal table (IEEE division without it or
+// where the table holds NaN), f64 absmax, s = m / 127, codes rint(RN(xs / s))
+// by Markstein, int32 code sums, so q / s_a / rowsum are bit-identical to
+// quant_act_smoothed's. A row is split over the group (16-byte vectors gt,
+// gt + 128, ...); the code pass recomputes the quotients rather than holding
+// them. Returns the number of rows quantized.
+QQQ_DEVICE int quantize_rows_fused(const GemmParams& p, int grp, int ngroups, int gt, uint8_t* scratch, int bar_id) {
+  if ((int)blockIdx.x >= p.q_ctas) return 0;
+  const int64_t nv = p.K / 8;
+  const int wq = gt >> 5, lane = gt & 31;
+#ifdef QQQ_EXP_FQ_NOWORK
+  { int r = 0; for (int row = (int)blockIdx.x + p.q_ctas * grp; row < p.M; row += p.q_ctas * ngroups) ++r; return r; }
+#endif
+  double* red = reinterpret_cast<double*>(scratch);  // [4] per-warp maxima
+  int* ired = reinterpret_cast<int*>(scratch + 32);   // [4] per-warp code sums
+  int rows = 0;
+#pragma unroll 1
+  for (int row = (int)blockIdx.x + p.q_ctas * grp; row < p.M; row += p.q_ctas * ngroups) {
+    const uint4* xr = reinterpret_cast<const uint4*>(p.xsrc + (int64_t)row * p.ldx);
+    double m = 0.0;
+    bool bad = false;
+#pragma unroll 1
+    for (int64_t i = gt; i < nv; i += 128) {
+      double xs[8];
+      smooth8(__ldg(xr + i), p.smooth, p.srecip, i, xs);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const double a = fabs(xs[t]);
+        bad |= is_bad(a);
+        m = a > m ? a : m;
+      }
+    }
+    if (bad) atomicOr(p.status, kStatNonFinite);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double t = __shfl_xor_sync(0xffffffffu, m, o);
+      m = t > m ? t : m;
+    }
+    if (lane == 0) red[wq] = m;
+    named_bar_sync(bar_id, 128);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) m = red[w] > m ? red[w] : m;
+    const double s = (m > 0.0) ? m / 127.0 : 1.0;
+    const double rs = 1.0 / s;
+    const bool ieee = !markstein_safe(s);
+    int8_t* qr = p.qdst + (int64_t)row * p.ldq;
+    int csum = 0;
+#pragma unroll 1
+    for (int64_t i = gt; i < nv; i += 128) {
+      double xs[8];
+      smooth8(__ldg(xr + i), p.smooth, p.srecip, i, xs);
+#ifdef QQQ_EXP_FQ_NOSTORE
+      const uint2 cc = codes8_f64(xs, s, rs, ieee, csum);
+      if (cc.x == 0x12345678u && cc.y == 0x9abcdef0u) *reinterpret_cast<uint2*>(qr + i * 8) = cc;
+#else
+      *reinterpret_cast<uint2*>(qr + i * 8) = codes8_f64(xs, s, rs, ieee, csum);
+#endif
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+    if (lane == 0) ired[wq] = csum;
+    named_bar_sync(bar_id, 128);
+    if (gt == 0) {
+      p.sa_dst[row] = s;
+      p.rs_dst[row] = ired[0] + ired[1] + ired[2] + ired[3];
+    }
+    ++rows;
+  }
+  return rows;
+}
+
+// Publish this group's rows: the codes were written through the generic proxy
+// and are read by other CTAs' tensor TMA (async proxy): proxy fence per
+// writer, group barrier, one gpu-scope release of the row count.
+QQQ_DEVICE void publish_rows_fused(const GemmParams& p, int rows, int gt, int bar_id) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  named_bar_sync(bar_id, 128);
+  if (gt == 0 && rows > 0)
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p.counters + kQRowsSlot), "r"(rows) : "memory");
+}
+
+// Wait until all M rows are published (acquire), then order this thread's
+// later async-proxy (TMA) reads after it. Co-residency: only CTAs of the first
+// wave quantize and they wait on nothing before publishing.
+QQQ_DEVICE void wait_rows_fused(const GemmParams& p) {
+#ifdef QQQ_EXP_FQ_NOWAIT
+  return;
+#endif
+  const int32_t* c = p.counters + kQRowsSlot;
+  unsigned long long t0 = 0;
+#pragma unroll 1
+  for (uint32_t n = 0;; ++n) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    if (v >= p.M) break;
+    __nanosleep(32);
+#ifndef QQQ_NO_WATCHDOG
+    if ((n & 1023) == 1023) {
+      const unsigned long long t = gtimer();
+      if (t0 == 0)
+        t0 = t;
+      else if (t - t0 > QQQ_WATCHDOG_NS)
+        __trap();
+    }
+#endif
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+#ifdef QQQ_EXP_FUSED_SLEEP
+  { const unsigned long long t1 = gtimer(); while (gtimer() - t1 < 20000) __nanosleep(500); }
+#endif
 }
 
 // Dequant epilogue for up to 16 consecutive tokens of one output channel n:
@@ -634,6 +774,10 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       if (++wi == C::kWStages) wi = 0;
     }
     griddep_wait();  // the int8 activations come from the previous kernel
+    if (p.xsrc) {  // ... or from this kernel's fused quantization
+      if (lane == 0) wait_rows_fused(p);
+      __syncwarp();
+    }
     for (int i = 0; i < C::kXStages && i < total; ++i) issue_x();
     uint32_t ws = 0, wph = 0, xs = 0, xph = 0;
 #pragma unroll 1
@@ -699,6 +843,10 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
   } else if (warp == C::kActProducerWarp) {
     // ================== activation producer (3-D tensor TMA) ==================
     griddep_wait();  // the int8 activations come from the previous kernel
+    if (p.xsrc) {  // ... or from this kernel's fused quantization
+      if (lane == 0) wait_rows_fused(p);
+      __syncwarp();
+    }
     if (lane == 0) QQQ_STAMP(3);
     SegIter si = make_iter(p);
     int tile, kb0, kb1;
@@ -884,10 +1032,13 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           }
           // Release the packed stage as soon as its bytes are in registers (before
           // the conversion), so the producer refills it one conversion earlier.
-          // The arrive must not issue before the loads have RETURNED (an empty asm
-          // consuming a register emits no instruction, so it does not wait): fold
-          // the last word of every slab (and the scales) into a zero offset of the
-          // barrier address, which makes the arrive data-dependent on every load.
+          // The arrive must not issue before the loads have RETURNED (LDS is
+          // asynchronous: an arrive without a data dependency lets the producer's
+          // next copy overwrite the stage under loads still in flight, which
+          // corrupted one TMEM lane quadrant's A rows now and then): fold the last
+          // word of every slab (and the scales) into a zero offset of the barrier
+          // address. The zero must be opaque to ptxas (p.zero): it folded a
+          // literal `and 0` and issued the arrive right behind the loads.
           {
             uint32_t dep = 0;
 #pragma unroll
@@ -899,7 +1050,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             asm volatile("" ::"r"(dep));
             dep = 0;
 #else
-            asm volatile("and.b32 %0, %0, 0;" : "+r"(dep));
+            asm volatile("and.b32 %0, %0, %1;" : "+r"(dep) : "r"(p.zero));
 #endif
             // one arrive per warp (the loads are one instruction per slab for the
             // whole warp, so lane 0's data dependency covers every lane).
@@ -1013,6 +1164,18 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       }
     }
     griddep_wait();  // y / acc / workspace / counters / s_a may belong to the previous kernel
+#ifdef QQQ_EXP_EPI_DELAY
+    { const unsigned long long t1 = gtimer(); while (gtimer() - t1 < QQQ_EXP_EPI_DELAY) __nanosleep(200); }
+#endif
+    if (p.xsrc) {
+      // fused smoothed quantization: this group's token rows, then wait for all of them
+      const int gq = warp - C::kEpiWarp0;
+      const int grp = gq >> 2, gt = (gq & 3) * 32 + lane;
+      const int rows = quantize_rows_fused(p, grp, C::kEpiGroups, gt, smem + C::kOffY + (grp * 4) * 2048, 2 + grp);
+      publish_rows_fused(p, rows, gt, 2 + grp);
+      if (threadIdx.x == C::kEpiWarp0 * 32) wait_rows_fused(p);
+      named_bar_sync(1, C::kNumEpiWarps * 32);
+    }
     const int et = threadIdx.x - C::kEpiWarp0 * 32;  // 0..kAll-1
     const bool lead = et == 0;                    // segment-level lead (counters)
     const bool hlead = (et & 127) == 0;           // half lead (TMA stores, partial prefetch)
@@ -1037,8 +1200,11 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       // stage this tile's per-token scales (and code sums) while the MMAs run
       named_bar_sync(kBarAll, kAll);  // previous segment done reading sa_smem / rs_smem
       for (int t = et; t < tvalid; t += kAll) {
-        sa_smem[t] = p.s_a[tok0 + t];
-        if constexpr (C::kU8) rs_smem[t] = 128 * p.rowsum[tok0 + t];
+        // (L2-coherent loads: with the fused quantization these are written in this
+        // launch by other CTAs; a const-pointer load may compile to the
+        // non-coherent path and be hoisted above the acquire)
+        sa_smem[t] = __ldcg(p.s_a + tok0 + t);
+        if constexpr (C::kU8) rs_smem[t] = 128 * __ldcg(p.rowsum + tok0 + t);
       }
       named_bar_sync(kBarAll, kAll);
       const int n = n_tile * 128 + row;
@@ -1478,6 +1644,15 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     __syncthreads();
   }
   if (threadIdx.x == 0) QQQ_STAMP(42);
+  if (p.xsrc && threadIdx.x == 0) {
+    // the last CTA done with the fused-quantization counter re-arms it
+    int prev;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(p.counters + kQDoneSlot) : "memory");
+    if (prev == (int)gridDim.x - 1) {
+      asm volatile("st.relaxed.gpu.global.s32 [%0], 0;" ::"l"(p.counters + kQRowsSlot) : "memory");
+      asm volatile("st.relaxed.gpu.global.s32 [%0], 0;" ::"l"(p.counters + kQDoneSlot) : "memory");
+    }
+  }
   if (warp == C::kAllocWarp) {
     tc_fence_after();
     if constexpr (PAIR)
@@ -1998,10 +2173,20 @@ extern "C" int qqq_gemm_plan_info(int mode, int64_t M, int64_t N, int64_t K, con
 }
 
 // Generic entry: mode 0 = per-channel (PC), 1 = per-group (PG), 2 = pre-converted int8 (I8).
-extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const int32_t* rowsum,
-                                const void* w_repacked, int64_t group, const double* s_col, int64_t M, int64_t N,
-                                int64_t K, void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace,
-                                size_t ws_bytes, const qqq_gemm_config* cfg, cudaStream_t stream) {
+namespace qqq {
+// fused smoothed quantization inputs (qqq_w4a8_gemm_smooth_fused)
+struct FusedQuantArgs {
+  const void* x;
+  int64_t ldx;
+  const double* smooth;
+  const double* recip;
+  int32_t* status;
+};
+
+static int gemm_launch(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const int32_t* rowsum,
+                       const void* w_repacked, int64_t group, const double* s_col, int64_t M, int64_t N, int64_t K,
+                       void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
+                       const qqq_gemm_config* cfg, cudaStream_t stream, const FusedQuantArgs* fq) {
   if (M < 0 || N <= 0 || K <= 0) return kErrShape;
   if (K > (1 << 16)) return kErrShape;  // gemm.py:49,151
   if (M == 0) return kOk;
@@ -2017,7 +2202,7 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
 
   LaunchPlan lp = make_plan(mode, M, N, K, cfg ? cfg->ntok : 0, cfg ? cfg->grid : 0, cfg ? cfg->split : -1,
                             cfg ? cfg->csplit : 0);
-  if (lp.tiles * (lp.pair ? 2 : 1) > kMaxTiles || lp.units > 0x7fffffff) return kErrUnsupported;
+  if (lp.tiles * (lp.pair ? 2 : 1) > (fq ? kQRowsSlot : kMaxTiles) || lp.units > 0x7fffffff) return kErrUnsupported;
   if (ws_bytes < plan_ws_bytes(lp)) return kErrConfig;
 
   CUtensorMap map;
@@ -2082,6 +2267,18 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
   p.pair = lp.pair;
   p.csplit = lp.csplit;
   p.dbg = cfg ? (unsigned long long*)cfg->dbg : nullptr;
+  if (fq) {
+    p.xsrc = (const __half*)fq->x;
+    p.ldx = fq->ldx;
+    p.smooth = fq->smooth;
+    p.srecip = fq->recip;
+    p.qdst = const_cast<int8_t*>(aq);
+    p.ldq = ldq;
+    p.sa_dst = const_cast<double*>(s_a);
+    p.rs_dst = const_cast<int32_t*>(rowsum);
+    p.status = fq->status;
+    p.q_ctas = std::min(lp.grid, num_sms());  // CTAs of the first wave (co-resident)
+  }
 
   if (lp.pair) {
     switch (mode) {
@@ -2096,6 +2293,36 @@ extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const d
     case kModeI8: return launch_mode<kModeI8>(lp.ntok, map, ymap, p, lp.grid, stream);
     default: return kErrConfig;
   }
+}
+
+}  // namespace qqq
+
+extern "C" int qqq_w4a8_gemm_ex(int mode, const int8_t* aq, int64_t ldq, const double* s_a, const int32_t* rowsum,
+                                const void* w_repacked, int64_t group, const double* s_col, int64_t M, int64_t N,
+                                int64_t K, void* y, int64_t ldy, int32_t* acc_opt, int64_t ldacc, void* workspace,
+                                size_t ws_bytes, const qqq_gemm_config* cfg, cudaStream_t stream) {
+  return gemm_launch(mode, aq, ldq, s_a, rowsum, w_repacked, group, s_col, M, N, K, y, ldy, acc_opt, ldacc, workspace,
+                     ws_bytes, cfg, stream, nullptr);
+}
+
+// apply_quant_linear's activation step fused into the GEMM (pipeline.py:144-152):
+// quantize x / smooth (fp16 [M, K]) into (q, s_a, rowsum) exactly as
+// qqq_act_quant_smooth(_rcp) does, inside the GEMM launch, then the GEMM on them.
+extern "C" int qqq_w4a8_gemm_smooth_fused(int mode, const void* x, int64_t ldx, const double* smooth,
+                                          const double* smooth_recip, int8_t* q, int64_t ldq, double* s_a,
+                                          int32_t* rowsum, int32_t* status_dev, const void* w_repacked, int64_t group,
+                                          const double* s_col, int64_t M, int64_t N, int64_t K, void* y, int64_t ldy,
+                                          int32_t* acc_opt, int64_t ldacc, void* workspace, size_t ws_bytes,
+                                          const qqq_gemm_config* cfg, cudaStream_t stream) {
+  if (mode != kModePC && mode != kModePG) return kErrConfig;
+  if (!x || !smooth || !q || !s_a || !rowsum || !status_dev) return kErrConfig;
+  if (M > 0 && (K % 8 != 0 || ldx % 8 != 0 || ldx < K || (reinterpret_cast<uintptr_t>(x) & 15) != 0 ||
+                (reinterpret_cast<uintptr_t>(smooth) & 15) != 0 ||
+                (smooth_recip && (reinterpret_cast<uintptr_t>(smooth_recip) & 15) != 0)))
+    return kErrUnsupported;
+  const FusedQuantArgs fq{x, ldx, smooth, smooth_recip, status_dev};
+  return gemm_launch(mode, q, ldq, s_a, rowsum, w_repacked, group, s_col, M, N, K, y, ldy, acc_opt, ldacc, workspace,
+                     ws_bytes, cfg, stream, &fq);
 }
 
 extern "C" int qqq_w4a8_gemm_pc(const int8_t* aq, int64_t ldq, const double* s_a, const void* w_repacked,
