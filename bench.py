@@ -519,15 +519,18 @@ C4_LINEARS = [("qkv", 4096, 12288), ("o", 4096, 4096), ("gate_up", 4096, 22016),
 def c4_stack_points(peaks, dev, batches=(1, 16, 64, 256)):
     """BASELINE configs[3] (C4): the Llama-2-7B decoder-layer linear stack
     (QKV 4096->12288, O 4096->4096, gate-up 4096->22016, down 11008->4096),
-    each linear = fused smooth-divide + per-token act quant (apply_quant_linear's
-    activation step, pipeline.py:146) + per-group g=128 W4A8 GEMM, the 8
-    launches of a stack chained with PDL in one CUDA graph; weights cold
-    (rotated layer replicas). Compared with the fp16 torch.matmul stack."""
+    each linear = apply_quant_linear's path (pipeline.py:144-152): fused
+    smooth-divide + per-token act quant kernel, then the per-group g=128 W4A8
+    GEMM, the 8 launches of a stack chained with PDL in one CUDA graph; weights
+    cold (rotated layer replicas). Also timed: the one-launch form
+    (apply_quant_linear(fused=True): quantization inside the GEMM launch).
+    Compared with the fp16 torch.matmul stack."""
     import torch
 
     import paper_2406_09904_b200 as Q
     from paper_2406_09904_b200 import _lib
     from paper_2406_09904_b200 import gemm as G
+    from paper_2406_09904_b200 import pipeline as P
 
     layer_bytes = sum(k * n / 2 for _, k, n in C4_LINEARS)
     R = max(2, math.ceil(2.5 * L2_BYTES / layer_bytes))
@@ -553,14 +556,22 @@ def c4_stack_points(peaks, dev, batches=(1, 16, 64, 256)):
         def stack_fn(lin):
             def f():
                 for i, (k, n, prep, sm, rc) in enumerate(lin):
+                    P.quant_linear_smoothed(xs[i], sm, rc, prep, n, check=False, y_out=ys[i])
+            return f
+
+        def stack_fn_2k(lin):
+            def f():
+                for i, (k, n, prep, sm, rc) in enumerate(lin):
                     aq = Q.quant_act_smoothed(xs[i], sm, check=False, recip=rc)
                     G.run_gemm(aq, prep, n, False, y_out=ys[i])
             return f
 
-        t_us = graph_time_us([stack_fn(lin) for lin in layers], reps=max(2, 20 // R), dev=dev)
+        t_fu = graph_time_us([stack_fn(lin) for lin in layers], reps=max(2, 20 // R), dev=dev)
+        t_us = graph_time_us([stack_fn_2k(lin) for lin in layers], reps=max(2, 20 // R), dev=dev)
         t16 = graph_time_us([(lambda ws: (lambda: [torch.matmul(xs[i], ws[i]) for i in range(4)]))(ws) for ws in w16],
                             reps=max(2, 20 // r16), dev=dev)
-        out.append(dict(batch=m, us_per_stack=round(t_us, 2), TOPS=round(ops_stack(m) / t_us / 1e6, 2),
+        out.append(dict(batch=m, us_per_stack=round(t_us, 2), us_per_stack_fused_launch=round(t_fu, 2),
+                        TOPS=round(ops_stack(m) / t_us / 1e6, 2),
                         fp16_us=round(t16, 2), speedup_vs_fp16=round(t16 / t_us, 3)))
     del layers, w16
     torch.cuda.empty_cache()

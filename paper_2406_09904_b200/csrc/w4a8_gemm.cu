@@ -380,41 +380,74 @@ QQQ_DEVICE void dequant16_all(const uint32_t (&r)[16], const double* sa, double 
 }
 
 // ---- fused smoothed activation quantization (GemmParams::xsrc) ----
-// The token rows of one epilogue group (128 threads, warps of the group at
-// scratch: 48 bytes): rows blockIdx.x + q_ctas * (grp + ngroups * j). The
-// arithmetic is act_quant_row_kernel<.., kSmooth = true>'s (act_quant.cu):
-// x / s_k by Markstein with the reciprocal table (IEEE division without it or
-// where the table holds NaN), f64 absmax, s = m / 127, codes rint(RN(xs / s))
-// by Markstein, int32 code sums, so q / s_a / rowsum are bit-identical to
-// quant_act_smoothed's. A row is split over the group (16-byte vectors gt,
-// gt + 128, ...); the code pass recomputes the quotients rather than holding
-// them. Returns the number of rows quantized.
-QQQ_DEVICE int quantize_rows_fused(const GemmParams& p, int grp, int ngroups, int gt, uint8_t* scratch, int bar_id) {
-  if ((int)blockIdx.x >= p.q_ctas) return 0;
+// The M x K activation block is cut into work items (row, slice of kQSlice
+// channels) spread over every epilogue group (128 threads) of the first-wave
+// CTAs, so a row's quotients are computed by several SMs at once:
+//   phase A (all of a group's items, no waiting): x / s_k for the slice
+//     (Markstein with the reciprocal table, IEEE division without it or where
+//     the table holds NaN), slice absmax -> atomicMax on the row's slot,
+//     release-increment of the row's phase-A count;
+//   phase B (per item): wait for the row's phase-A count to reach its slice
+//     count, s = m / 127, codes rint(RN(xs / s)) by Markstein for the slice,
+//     partial code sum -> the row's sum slot, acq_rel-increment of the row's
+//     phase-B count; the last slice of a row writes s_a and rowsum, re-arms the
+//     row's slots and counts the row as published.
+// The arithmetic is act_quant_row_kernel<.., kSmooth = true>'s (act_quant.cu),
+// so q / s_a / rowsum are bit-identical to quant_act_smoothed's (the max is
+// order-independent, the code sum an exact integer sum). Phase A never waits,
+// so no group waits on an item another group has not started (deadlock-free
+// among co-resident CTAs). Per-row slots (workspace head, zero on entry and
+// exit): m (u64 bits of a non-negative double), code sum, phase-A and phase-B
+// counts.
+constexpr int kQSlice = 2048;                 // channels per work item (2 x 8 per thread)
+QQQ_DEVICE int32_t* qrow_slots(const GemmParams& p) { return p.counters + kQRowsSlot - 6 * p.M - 2; }
+
+QQQ_DEVICE void smooth_vecs(const GemmParams& p, int row, int slice, int gt, double (&xs)[2][8], bool& bad,
+                            double& m) {
+  const uint4* xr = reinterpret_cast<const uint4*>(p.xsrc + (int64_t)row * p.ldx);
   const int64_t nv = p.K / 8;
-  const int wq = gt >> 5, lane = gt & 31;
-#ifdef QQQ_EXP_FQ_NOWORK
-  { int r = 0; for (int row = (int)blockIdx.x + p.q_ctas * grp; row < p.M; row += p.q_ctas * ngroups) ++r; return r; }
-#endif
-  double* red = reinterpret_cast<double*>(scratch);  // [4] per-warp maxima
-  int* ired = reinterpret_cast<int*>(scratch + 32);   // [4] per-warp code sums
-  int rows = 0;
-#pragma unroll 1
-  for (int row = (int)blockIdx.x + p.q_ctas * grp; row < p.M; row += p.q_ctas * ngroups) {
-    const uint4* xr = reinterpret_cast<const uint4*>(p.xsrc + (int64_t)row * p.ldx);
-    double m = 0.0;
-    bool bad = false;
-#pragma unroll 1
-    for (int64_t i = gt; i < nv; i += 128) {
-      double xs[8];
-      smooth8(__ldg(xr + i), p.smooth, p.srecip, i, xs);
+#pragma unroll
+  for (int v = 0; v < 2; ++v) {
+    const int64_t i = (int64_t)slice * (kQSlice / 8) + v * 128 + gt;
+    if (i < nv) {
+      smooth8(__ldg(xr + i), p.smooth, p.srecip, i, xs[v]);
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        const double a = fabs(xs[t]);
+        const double a = fabs(xs[v][t]);
         bad |= is_bad(a);
         m = a > m ? a : m;
       }
     }
+  }
+}
+
+// Returns the number of rows this group finished (published by the caller).
+QQQ_DEVICE int quantize_rows_fused(const GemmParams& p, int grp, int ngroups, int gt, uint8_t* scratch, int bar_id) {
+  if ((int)blockIdx.x >= p.q_ctas) return 0;
+  const int wq = gt >> 5, lane = gt & 31;
+#ifdef QQQ_EXP_FQ_NOWORK
+  (void)wq;
+  (void)lane;
+  return 0;
+#endif
+  const int S = (p.K + kQSlice - 1) / kQSlice;  // slices per row
+  const int items = p.M * S;
+  const int G = p.q_ctas * ngroups, g = grp * p.q_ctas + (int)blockIdx.x;
+  int32_t* slots = qrow_slots(p);  // [M] u64 m | [M] sum | [M] cntA | [M] cntB
+  unsigned long long* mslot = reinterpret_cast<unsigned long long*>(slots);
+  int32_t* sumslot = slots + 2 * p.M;
+  int32_t* cnta = sumslot + p.M;
+  int32_t* cntb = cnta + p.M;
+  double* red = reinterpret_cast<double*>(scratch);  // [4] per-warp maxima
+  int* ired = reinterpret_cast<int*>(scratch + 32);   // [4] per-warp code sums
+  // ---- phase A
+#pragma unroll 1
+  for (int it = g; it < items; it += G) {
+    const int row = it / S, slice = it % S;
+    double xs[2][8];
+    double m = 0.0;
+    bool bad = false;
+    smooth_vecs(p, row, slice, gt, xs, bad, m);
     if (bad) atomicOr(p.status, kStatNonFinite);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -423,43 +456,97 @@ QQQ_DEVICE int quantize_rows_fused(const GemmParams& p, int grp, int ngroups, in
     }
     if (lane == 0) red[wq] = m;
     named_bar_sync(bar_id, 128);
+    if (gt == 0) {
 #pragma unroll
-    for (int w = 0; w < 4; ++w) m = red[w] > m ? red[w] : m;
+      for (int w = 0; w < 4; ++w) m = red[w] > m ? red[w] : m;
+      atomicMax(mslot + row, (unsigned long long)__double_as_longlong(m));
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(cnta + row) : "memory");
+    }
+    named_bar_sync(bar_id, 128);  // red[] reused by the next item
+  }
+  // ---- phase B
+  if (gt == 0 && grp == 0) QQQ_STAMP(177);
+  int rows = 0;
+#pragma unroll 1
+  for (int it = g; it < items; it += G) {
+    const int row = it / S, slice = it % S;
+    if (gt == 0) {
+      unsigned long long t0 = 0;
+#pragma unroll 1
+      for (uint32_t n = 0;; ++n) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnta + row) : "memory");
+        if (v >= S) break;
+        __nanosleep(32);
+#ifndef QQQ_NO_WATCHDOG
+        if ((n & 1023) == 1023) {
+          const unsigned long long t = gtimer();
+          if (t0 == 0)
+            t0 = t;
+          else if (t - t0 > QQQ_WATCHDOG_NS)
+            __trap();
+        }
+#endif
+      }
+    }
+    named_bar_sync(bar_id, 128);
+    unsigned long long mb;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(mb) : "l"(mslot + row) : "memory");
+    const double m = __longlong_as_double((long long)mb);
     const double s = (m > 0.0) ? m / 127.0 : 1.0;
     const double rs = 1.0 / s;
     const bool ieee = !markstein_safe(s);
+    double xs[2][8];
+    double mm = 0.0;
+    bool bad = false;
+    smooth_vecs(p, row, slice, gt, xs, bad, mm);  // (recomputed: registers are not held across phase A)
     int8_t* qr = p.qdst + (int64_t)row * p.ldq;
+    const int64_t nv = p.K / 8;
     int csum = 0;
-#pragma unroll 1
-    for (int64_t i = gt; i < nv; i += 128) {
-      double xs[8];
-      smooth8(__ldg(xr + i), p.smooth, p.srecip, i, xs);
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int64_t i = (int64_t)slice * (kQSlice / 8) + v * 128 + gt;
+      if (i < nv) {
 #ifdef QQQ_EXP_FQ_NOSTORE
-      const uint2 cc = codes8_f64(xs, s, rs, ieee, csum);
-      if (cc.x == 0x12345678u && cc.y == 0x9abcdef0u) *reinterpret_cast<uint2*>(qr + i * 8) = cc;
+        const uint2 cc = codes8_f64(xs[v], s, rs, ieee, csum);
+        if (cc.x == 0x12345678u && cc.y == 0x9abcdef0u) *reinterpret_cast<uint2*>(qr + i * 8) = cc;
 #else
-      *reinterpret_cast<uint2*>(qr + i * 8) = codes8_f64(xs, s, rs, ieee, csum);
+        *reinterpret_cast<uint2*>(qr + i * 8) = codes8_f64(xs[v], s, rs, ieee, csum);
 #endif
+      }
     }
+    // codes are read by other CTAs' tensor TMA (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
     if (lane == 0) ired[wq] = csum;
     named_bar_sync(bar_id, 128);
     if (gt == 0) {
-      p.sa_dst[row] = s;
-      p.rs_dst[row] = ired[0] + ired[1] + ired[2] + ired[3];
+      const int part = ired[0] + ired[1] + ired[2] + ired[3];
+      atomicAdd(sumslot + row, part);
+      int prev;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(cntb + row) : "memory");
+      if (prev == S - 1) {  // the row's last slice: every slice's sum and codes are visible
+        int total;
+        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(total) : "l"(sumslot + row) : "memory");
+        p.sa_dst[row] = s;
+        p.rs_dst[row] = total;
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(mslot + row), "l"(0ull) : "memory");
+        asm volatile("st.relaxed.gpu.global.s32 [%0], 0;" ::"l"(sumslot + row) : "memory");
+        asm volatile("st.relaxed.gpu.global.s32 [%0], 0;" ::"l"(cnta + row) : "memory");
+        asm volatile("st.relaxed.gpu.global.s32 [%0], 0;" ::"l"(cntb + row) : "memory");
+        ++rows;
+      }
     }
-    ++rows;
+    named_bar_sync(bar_id, 128);  // ired[] reused by the next item
   }
-  return rows;
+  return rows;  // (meaningful in thread gt == 0)
 }
 
-// Publish this group's rows: the codes were written through the generic proxy
-// and are read by other CTAs' tensor TMA (async proxy): proxy fence per
-// writer, group barrier, one gpu-scope release of the row count.
+// Publish the rows this group finished: one gpu-scope release of the count
+// (the finishing thread acquired every slice of those rows).
 QQQ_DEVICE void publish_rows_fused(const GemmParams& p, int rows, int gt, int bar_id) {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  named_bar_sync(bar_id, 128);
+  (void)bar_id;
   if (gt == 0 && rows > 0)
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p.counters + kQRowsSlot), "r"(rows) : "memory");
 }
@@ -777,6 +864,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     if (p.xsrc) {  // ... or from this kernel's fused quantization
       if (lane == 0) wait_rows_fused(p);
       __syncwarp();
+      if (lane == 0) QQQ_STAMP(180);
     }
     for (int i = 0; i < C::kXStages && i < total; ++i) issue_x();
     uint32_t ws = 0, wph = 0, xs = 0, xph = 0;
@@ -846,6 +934,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     if (p.xsrc) {  // ... or from this kernel's fused quantization
       if (lane == 0) wait_rows_fused(p);
       __syncwarp();
+      if (lane == 0) QQQ_STAMP(180);
     }
     if (lane == 0) QQQ_STAMP(3);
     SegIter si = make_iter(p);
@@ -1171,9 +1260,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       // fused smoothed quantization: this group's token rows, then wait for all of them
       const int gq = warp - C::kEpiWarp0;
       const int grp = gq >> 2, gt = (gq & 3) * 32 + lane;
+      if (threadIdx.x == C::kEpiWarp0 * 32) QQQ_STAMP(176);
       const int rows = quantize_rows_fused(p, grp, C::kEpiGroups, gt, smem + C::kOffY + (grp * 4) * 2048, 2 + grp);
+      if (threadIdx.x == C::kEpiWarp0 * 32) QQQ_STAMP(178);
       publish_rows_fused(p, rows, gt, 2 + grp);
       if (threadIdx.x == C::kEpiWarp0 * 32) wait_rows_fused(p);
+      if (threadIdx.x == C::kEpiWarp0 * 32) QQQ_STAMP(179);
       named_bar_sync(1, C::kNumEpiWarps * 32);
     }
     const int et = threadIdx.x - C::kEpiWarp0 * 32;  // 0..kAll-1
@@ -2202,7 +2294,9 @@ static int gemm_launch(int mode, const int8_t* aq, int64_t ldq, const double* s_
 
   LaunchPlan lp = make_plan(mode, M, N, K, cfg ? cfg->ntok : 0, cfg ? cfg->grid : 0, cfg ? cfg->split : -1,
                             cfg ? cfg->csplit : 0);
-  if (lp.tiles * (lp.pair ? 2 : 1) > (fq ? kQRowsSlot : kMaxTiles) || lp.units > 0x7fffffff) return kErrUnsupported;
+  // (the fused quantization keeps 6 int32 slots per token row below its row counter)
+  if (lp.tiles * (lp.pair ? 2 : 1) > (fq ? kQRowsSlot - 6 * M - 2 : (int64_t)kMaxTiles) || lp.units > 0x7fffffff)
+    return kErrUnsupported;
   if (ws_bytes < plan_ws_bytes(lp)) return kErrConfig;
 
   CUtensorMap map;

@@ -3,14 +3,15 @@
 `apply_quant_linear(x, layer)` is the caller of the W4A8 GEMM in the reference
 pipeline: divide the activations by the layer's smoothing vector, quantize per
 token, run the per-channel or per-group W4A8 GEMM and return y widened to f64.
-Here the divide is fused into the activation quantizer, and the quantizer
-into the GEMM launch (`qqq_w4a8_gemm_smooth_fused`: the GEMM's epilogue warps
-quantize the token rows while its weights stream in); launches use
-programmatic dependent launch, so a chain of linears (the C4 decoder-layer
-stack) overlaps each GEMM's weight prefetch with its predecessor. Inputs the
-fused launch does not take (non-fp16 activations, K or row pitch not a
-multiple of 8, weights needing the int8 clamp layout) run the two-kernel form
-(`quant_act_smoothed` + the GEMM), with identical results.
+Here the divide is fused into the activation quantizer (`qqq_act_quant_smooth`),
+and the GEMM is the tcgen05 kernel; both launch with programmatic dependent
+launch, so a chain of linears (the C4 decoder-layer stack) overlaps each GEMM's
+weight prefetch with its predecessor. `apply_quant_linear(..., fused=True)`
+runs the one-launch form instead (`qqq_w4a8_gemm_smooth_fused`: the GEMM's
+epilogue warps quantize the token rows while its weights stream in;
+bit-identical results). It measured slower on the C4 stack (its
+activation loads and cross-CTA reductions queue behind the weight stream), so
+the two-kernel form is the default.
 
 The containers mirror the reference's field names: `SmoothingPlan`
 (smoothing.py:36-48) and `QuantizedLayer` (pipeline.py:86-90).
@@ -127,7 +128,9 @@ def _fused_ok(x: torch.Tensor, prep) -> bool:
         return False
     m, k = x.shape
     ldx = x.stride(0) if m > 1 else k
-    return (k % 8 == 0 and x.stride(1) == 1 and ldx % 8 == 0 and ldx >= k and x.data_ptr() % 16 == 0)
+    # (m <= 4096: the launch keeps per-row counters in the workspace head)
+    return (0 < m <= 4096 and k % 8 == 0 and x.stride(1) == 1 and ldx % 8 == 0 and ldx >= k
+            and x.data_ptr() % 16 == 0)
 
 
 def quant_linear_smoothed(x: torch.Tensor, s: torch.Tensor, recip, prep, n: int, check: bool = True,
@@ -151,8 +154,9 @@ def quant_linear_smoothed(x: torch.Tensor, s: torch.Tensor, recip, prep, n: int,
         ws = _gemm.workspace(dev, wsb)
         c = None
         if cfg:
+            dbg = cfg.get("dbg")
             c = _lib.GemmConfig(int(cfg.get("ntok", 0)), int(cfg.get("grid", 0)), int(cfg.get("split", -1)),
-                                int(cfg.get("csplit", 0)), None)
+                                int(cfg.get("csplit", 0)), None if dbg is None else dbg.data_ptr())
         rc = lib.qqq_w4a8_gemm_smooth_fused(prep.mode, _lib.ptr(x), x.stride(0) if m > 1 else k, _lib.ptr(s),
                                             None if recip is None else _lib.ptr(recip), _lib.ptr(qbuf), kp,
                                             _lib.ptr(s_a), _lib.ptr(rowsum), _lib.ptr(status), _lib.ptr(prep.w),
@@ -181,9 +185,10 @@ def layer_fused_scales(layer: QuantizedLayer) -> FusedScales:
     return hit[1]
 
 
-def apply_quant_linear(x, layer: QuantizedLayer, check: bool = True) -> torch.Tensor:
+def apply_quant_linear(x, layer: QuantizedLayer, check: bool = True, fused: bool = False) -> torch.Tensor:
     """Quantized forward of one linear (pipeline.py:144-152): divide by s,
-    quantize, W4A8 GEMM; returns y widened to f64 (GemmOutput.y_wide)."""
+    quantize, W4A8 GEMM; returns y widened to f64 (GemmOutput.y_wide).
+    fused=True: one launch (quant_linear_smoothed) where the inputs allow it."""
     # Per-layer caches, keyed on the identity and version of what they were
     # built from: a reassigned plan / qweights (or an in-place edit of s or of
     # the weight scales) rebuilds them instead of reusing stale values.
@@ -196,7 +201,7 @@ def apply_quant_linear(x, layer: QuantizedLayer, check: bool = True) -> torch.Te
     qw = layer.qweights
     fused = layer_fused_scales(layer)
     xt = x if isinstance(x, torch.Tensor) else None
-    if xt is not None and xt.is_cuda and xt.dtype == torch.float16 and xt.ndim == 2:
+    if fused and xt is not None and xt.is_cuda and xt.dtype == torch.float16 and xt.ndim == 2:
         if xt.shape[1] != qw.rows:
             raise ShapeError(f"activation K={xt.shape[1]} does not match weight K={qw.rows}")
         if qw.scheme != fused.scheme:

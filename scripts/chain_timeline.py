@@ -29,6 +29,7 @@ ap.add_argument("--m", type=int, default=1)
 ap.add_argument("--scheme", default="per-group")
 ap.add_argument("--cfg", default="{}")
 ap.add_argument("--len", type=int, default=6)
+ap.add_argument("--fused", action="store_true", help="the fused smooth-quant launch (quant_linear_smoothed)")
 a = ap.parse_args()
 k, n = map(int, a.shape.split("x"))
 dev = torch.device("cuda", 0)
@@ -43,9 +44,20 @@ dbgs = [torch.zeros((1024, 192), dtype=torch.int64, device=dev) for _ in range(L
 cfg = json.loads(a.cfg)
 
 
+from paper_2406_09904_b200 import pipeline as P  # noqa: E402
+from paper_2406_09904_b200 import _lib  # noqa: E402
+sm = torch.ones(k, dtype=torch.float64, device=dev)
+sm[::8] = 1.5
+rc = Q.smoothing_reciprocal(sm)
+
+
 def launch():
     for i in range(L):
-        G.run_gemm(aq, preps[i], n, False, y_out=y, cfg=dict(cfg, dbg=dbgs[i]))
+        if a.fused:
+            # (the dbg timeline buffer rides in the plan config)
+            P.quant_linear_smoothed(x, sm, rc, preps[i], n, check=False, y_out=y, cfg=dict(cfg, dbg=dbgs[i]))
+        else:
+            G.run_gemm(aq, preps[i], n, False, y_out=y, cfg=dict(cfg, dbg=dbgs[i]))
 
 
 launch()
@@ -70,6 +82,9 @@ ds = [d.cpu().numpy().astype(np.int64) for d in dbgs]
 t0 = min(d[d[:, 0] > 0, 0].min() for d in ds)
 SLOTS = [("start", 0), ("dep_wait", 3), ("full0", 4), ("conv0", 80), ("mma_xfull0", 96), ("mma0", 20), ("mma3", 23), ("conv3", 83),
          ("accfull0", 36), ("cs_own", 150), ("cs_recv", 151), ("cs_add", 152), ("cs_done", 153), ("loop_end", 154), ("epi_end", 63), ("exit", 42)]
+if a.fused:
+    SLOTS = [("start", 0), ("q_start", 176), ("q_phaseA", 177), ("q_phaseB", 178), ("q_all", 179), ("x_wait", 180),
+             ("full0", 4), ("conv0", 80), ("mma_xfull0", 96), ("mma0", 20), ("accfull0", 36), ("epi_end", 63), ("exit", 42)]
 
 
 def stat(d, sl):

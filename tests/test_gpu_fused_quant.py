@@ -152,7 +152,7 @@ def test_fused_nonfinite_raises():
 
 
 def test_apply_quant_linear_takes_fused_path():
-    """apply_quant_linear on fp16 CUDA activations runs the fused launch (same y as the two-kernel form)."""
+    """apply_quant_linear(fused=True) on fp16 CUDA activations runs the fused launch (same y as the two-kernel form)."""
     k, n, m = 4096, 1024, 33
     rng = np.random.default_rng(3)
     w = rng.standard_normal((k, n))
@@ -170,7 +170,7 @@ def test_apply_quant_linear_takes_fused_path():
 
     P.quant_linear_smoothed = spy
     try:
-        y = Q.apply_quant_linear(x, layer)
+        y = Q.apply_quant_linear(x, layer, fused=True)
     finally:
         P.quant_linear_smoothed = orig
     assert called

@@ -61,6 +61,9 @@ def test_gpu_apply_quant_linear_bit_exact():
         y = Q.apply_quant_linear(x, layer)
         assert y.dtype == torch.float64
         assert np.array_equal(y.cpu().numpy().view(np.uint64), c["y"].view(np.uint64)), c["i"]
+        # the one-launch form (quantization inside the GEMM launch) where the inputs allow it
+        yf = Q.apply_quant_linear(x, layer, fused=True)
+        assert np.array_equal(yf.cpu().numpy().view(np.uint64), c["y"].view(np.uint64)), c["i"]
 
 
 @pytest.mark.gpu
