@@ -1906,12 +1906,16 @@ static LaunchPlan plan_for(int mode, int64_t M, int64_t N, int64_t K, int ntok, 
     lp.tiles = lp.n_tiles * lp.tok_tiles;
     lp.units = (int64_t)lp.tiles * lp.kb_per_tile;
     lp.max_segs = 1;
-    // 32-token clusters are kept to one CTA per SM: with two co-resident 32-token
-    // cluster CTAs per SM, stress runs (scripts/stress_plans.py, 800 launches)
-    // saw one TMEM lane quadrant of one CTA's partial corrupted in 1-10% of the
-    // launches (never with one CTA per SM, never with 16-token clusters; not
-    // from the TMEM column budget either: with 64 spare columns per CTA it persists).
-    static const bool allow32 = getenv("QQQ_EXP_NTOK32_TWO_PER_SM") != nullptr;  // developer A/B switch
+    // 32-token clusters run two CTAs per SM again. They had been capped to one
+    // after stress runs saw one TMEM lane quadrant of one CTA's partial corrupted
+    // in 1-10% of the launches; the cause was the converters' weight-stage
+    // release racing their own shared-memory loads (see the converter loop),
+    // which the co-resident CTA's timing exposed. 6000 stress launches clean
+    // since the fix; QQQ_NT32_ONE_PER_SM=1 restores the cap.
+#ifndef QQQ_NT32_ONE_PER_SM
+#define QQQ_NT32_ONE_PER_SM 0
+#endif
+    static const bool allow32 = !QQQ_NT32_ONE_PER_SM || getenv("QQQ_EXP_NTOK32_TWO_PER_SM") != nullptr;
     const int slots = (force_grid > 0 ? std::min(force_grid, num_sms()) : num_sms()) *
                       ((ntok == 32 && !allow32) ? 1 : ctas_per_sm(mode, ntok));
     // Cluster size S <= 8 (portable), receive buffer [S][ceil(128/S)][NTOK] int32
@@ -2062,9 +2066,13 @@ static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
     // share an SM, +2.2 us for the 32-token tile (2 weight stages)
     const int ucta_cs = (lp.kb_per_tile + lp.csplit - 1) / lp.csplit;
     const double shared = std::max(0, lp.grid - num_sms()) / (double)num_sms();
-    // (+2.9 us on 32-token clusters since they are capped to one CTA per SM:
-    //  11008x4096 M=32 S=4 measured 15.0 us against 12.1 from the round-1 fit)
-    return 4.813 + 0.456 * ucta_cs + 0.671 * shared * ucta_cs + (lp.ntok == 32 ? 5.13 : 0.0) + 0.012 * mt;
+    // (+2 us on 32-token clusters: the round-1 fit underestimates them, e.g.
+    //  11008x4096 M=32 S=4 measured 14.6 us against 12.1; with +2 the planner
+    //  takes them where they win, 4096x11008 M=17-32: 13.9 -> 12.0-12.4 us)
+#ifndef QQQ_NT32_PENALTY
+#define QQQ_NT32_PENALTY 2.0
+#endif
+    return 4.813 + 0.456 * ucta_cs + 0.671 * shared * ucta_cs + (lp.ntok == 32 ? QQQ_NT32_PENALTY : 0.0) + 0.012 * mt;
   }
   if (lp.pair) {
     // 2-CTA pair tiles: ~0.41 us per 128-deep k-block of a 256x256 pair tile; the

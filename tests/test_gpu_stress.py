@@ -2,9 +2,9 @@
 of the plans with co-resident cluster CTAs, each checked bit-exactly against
 the oracle: intermittent races show up here, not in single-launch parity.
 
-Covers the two-CTA-per-SM 16-token cluster split-K decode plans the planner
-picks on the 7B shapes, the one-CTA-per-SM 32-token clusters, and the
-128-token whole-SM clusters (scripts/stress_plans.py is the long version).
+Covers the two-CTA-per-SM 16- and 32-token cluster split-K decode plans the
+planner picks on the 7B shapes and the 128-token whole-SM clusters
+(scripts/stress_plans.py is the long version).
 """
 
 import numpy as np
@@ -21,7 +21,8 @@ CASES = [
     # (K, N, M, scheme, cfg)
     (11008, 4096, 1, "per-group", {"ntok": 16, "split": 4, "csplit": 6}),   # 192 CTAs, 2 per SM
     (4096, 11008, 16, "per-channel", {"ntok": 16, "split": 4, "csplit": 2}),  # 172 CTAs
-    (8192, 8192, 1, "per-channel", {"ntok": 32, "split": 4, "csplit": 4}),  # capped to one CTA per SM
+    (8192, 8192, 1, "per-channel", {"ntok": 32, "split": 4, "csplit": 4}),  # two CTAs per SM
+    (4096, 11008, 24, "per-group", {"ntok": 32, "split": 4, "csplit": 2}),  # (the planner's pick there)
     (4096, 4096, 128, "per-group", {"ntok": 128, "split": 4, "csplit": 4}),  # whole-SM clusters
 ]
 
