@@ -313,7 +313,7 @@ QQQ_DEVICE void st_async_b32(uint32_t cl_addr, uint32_t v, uint32_t cl_bar) {
 // division). The CTAs exchange their partial absmax (st.async into every
 // peer's shared memory, completing on its mbarrier) and their code sums (into
 // rank 0, which writes s_a and rowsum). Same arithmetic as the row kernel.
-template <int kThreads, bool kSmooth>
+template <int kThreads, bool kSmooth, int kVPT = 1>
 __global__ void __launch_bounds__(kThreads) act_quant_cluster_kernel(const __half* __restrict__ x, int64_t K,
                                                                       int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
                                                                       double* __restrict__ s_out, int32_t* status,
@@ -338,26 +338,36 @@ __global__ void __launch_bounds__(kThreads) act_quant_cluster_kernel(const __hal
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t nv = K / 8;
   const int64_t v0 = rank * nv / G, v1 = (rank + 1) * nv / G;
-  const int64_t i = v0 + threadIdx.x;
-  const bool has = i < v1;
-  uint4 v = has ? __ldg(reinterpret_cast<const uint4*>(x + row * ldx) + i) : make_uint4(0, 0, 0, 0);
-  const __half* e = reinterpret_cast<const __half*>(&v);
-  double xs[8];
-  if constexpr (kSmooth) {
-    if (has) {
-      smooth8(v, smooth, recip, i, xs);
-    } else {
+  // kVPT 16-byte vectors per thread: v0 + threadIdx.x + j * kThreads (all loads first)
+  uint4 v[kVPT];
+  bool has[kVPT];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) xs[t] = 0.0;
-    }
+  for (int j = 0; j < kVPT; ++j) {
+    const int64_t i = v0 + threadIdx.x + (int64_t)j * kThreads;
+    has[j] = i < v1;
+    v[j] = has[j] ? __ldg(reinterpret_cast<const uint4*>(x + row * ldx) + i) : make_uint4(0, 0, 0, 0);
   }
+  double xs[kSmooth ? kVPT : 1][8];
   Acc m = Acc(0);
   bool bad = false;
 #pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const Acc a = kSmooth ? (Acc)fabs(xs[t]) : (Acc)fabsf(__half2float(e[t]));
-    bad |= is_bad(a);
-    m = a > m ? a : m;
+  for (int j = 0; j < kVPT; ++j) {
+    const int64_t i = v0 + threadIdx.x + (int64_t)j * kThreads;
+    const __half* e = reinterpret_cast<const __half*>(&v[j]);
+    if constexpr (kSmooth) {
+      if (has[j]) {
+        smooth8(v[j], smooth, recip, i, xs[j]);
+      } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) xs[j][t] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const Acc a = kSmooth ? (Acc)fabs(xs[kSmooth ? j : 0][t]) : (Acc)fabsf(__half2float(e[t]));
+      bad |= is_bad(a);
+      m = a > m ? a : m;
+    }
   }
   if (__syncthreads_or(bad)) {
     if (threadIdx.x == 0) atomicOr(status, kStatNonFinite);
@@ -382,13 +392,17 @@ __global__ void __launch_bounds__(kThreads) act_quant_cluster_kernel(const __hal
   const float inv = zero_row ? 0.0f : 127.0f / (float)mr;
   const double rs = 1.0 / s;
   int csum = 0;
-  if (has) {
-    uint2 o;
-    if constexpr (kSmooth)
-      o = codes8_f64(xs, s, rs, !markstein_safe(s), csum);
-    else
-      o = codes8_f16(v, inv, s, rs, csum);
-    *reinterpret_cast<uint2*>(q + row * ldq + i * 8) = o;
+#pragma unroll
+  for (int j = 0; j < kVPT; ++j) {
+    if (has[j]) {
+      const int64_t i = v0 + threadIdx.x + (int64_t)j * kThreads;
+      uint2 o;
+      if constexpr (kSmooth)
+        o = codes8_f64(xs[j], s, rs, !markstein_safe(s), csum);
+      else
+        o = codes8_f16(v[j], inv, s, rs, csum);
+      *reinterpret_cast<uint2*>(q + row * ldq + i * 8) = o;
+    }
   }
   for (int o = 16; o > 0; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
   if ((threadIdx.x & 31) == 0) isum[threadIdx.x >> 5] = csum;
@@ -450,20 +464,29 @@ static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, in
   // M <= 256 (decode and mid batches), smoothed fp16 rows up to 8 x 256 vectors: row split over
   // a cluster (measured: 4.7 vs 5.2 us per smoothed M=1 quantizer in the C4 chain; the
   // plain quantizer's ~35 instructions per element gain nothing from it)
-  constexpr int kCT = 256;
+#ifndef QQQ_QCLUSTER_CT
+#define QQQ_QCLUSTER_CT 256
+#endif
+#ifndef QQQ_QCLUSTER_VPT
+#define QQQ_QCLUSTER_VPT 1
+#endif
+  constexpr int kCT = QQQ_QCLUSTER_CT, kCV = QQQ_QCLUSTER_VPT;
   // The reciprocal table replaces the per-element division routine by 5 FMA-pipe
   // ops but adds a 64-byte table read per 8 channels: a win for decode batches
   // (C4 stack quantizers 16.5 -> 14.7 us at M = 1..16), a loss from M ~ 64 on
   // (33.0 -> 36.9 us at M = 256), where the kernel waits on loads, not issue.
-  constexpr int64_t kRecipMaxM = 32;
+#ifndef QQQ_RECIP_MAXM
+#define QQQ_RECIP_MAXM 32
+#endif
+  constexpr int64_t kRecipMaxM = QQQ_RECIP_MAXM;
 #ifndef QQQ_QCLUSTER_MAXM
 #define QQQ_QCLUSTER_MAXM 256
 #endif
   if (smooth && x_dtype == 0 && !row_max_in && !row_max_out && !smooth_mask && M <= QQQ_QCLUSTER_MAXM && K % 8 == 0 &&
-      K <= (int64_t)8 * kCT * 8 && ldx % 8 == 0 && ldq % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      K <= (int64_t)8 * kCT * kCV * 8 && ldx % 8 == 0 && ldq % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(q) & 7) == 0 && (reinterpret_cast<uintptr_t>(smooth) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(recip) & 15) == 0) {
-    const int G = (int)((K / 8 + kCT - 1) / kCT);
+    const int G = (int)((K / 8 + kCT * kCV - 1) / (kCT * kCV));
     cudaLaunchAttribute ca[2];
     ca[0] = attr[0];
     ca[1].id = cudaLaunchAttributeClusterDimension;
@@ -475,7 +498,7 @@ static int act_quant_launch(const void* x, int x_dtype, int64_t M, int64_t K, in
     cc.blockDim = dim3(kCT);
     cc.attrs = ca;
     cc.numAttrs = 2;
-    e = cudaLaunchKernelEx(&cc, act_quant_cluster_kernel<kCT, true>, (const __half*)x, K, ldx, q, ldq, s_a,
+    e = cudaLaunchKernelEx(&cc, act_quant_cluster_kernel<kCT, true, kCV>, (const __half*)x, K, ldx, q, ldq, s_a,
                            status_dev, rowsum, smooth, M <= kRecipMaxM ? recip : nullptr);
     return e == cudaSuccess ? kOk : kErrCuda;
   }
