@@ -214,7 +214,18 @@ struct Cfg {
   static constexpr int kXCapWanted = PAIR ? QQQ_PAIR_XCAP : kSmall ? QQQ_SMALL_XCAP : QQQ_BIG_XCAP;
   static constexpr int kXCap = kABufsMax < kXCapWanted ? kABufsMax : kXCapWanted;
   static constexpr int kXStages = kXStagesRaw < 2 ? 2 : (kXStagesRaw > kXCap ? kXCap : kXStagesRaw);
-  static constexpr int kABufs = kConvert ? kXStages : 0;
+  // Whole-tile plans of the whole-SM (non-pair) CTA borrow the split-K partial
+  // ring, idle when no tile is split, as one more activation stage (and TMEM A
+  // buffer): the k-block pace of these tiles is bound by the activation
+  // ring's latency, not by its bandwidth (runtime ring size: `nx` in the kernel).
+  static constexpr int kPartBytes = kEpiGroups * kPartBufs * 8192;
+#ifndef QQQ_XTRA_STAGE
+#define QQQ_XTRA_STAGE 1
+#endif
+  static constexpr int kXStagesXtra =
+      (QQQ_XTRA_STAGE && !kSmall && !PAIR && kConvert && kPartBytes >= kXBytes && kXStages + 1 <= kABufsMax) ? 1 : 0;
+  static constexpr int kXStagesMax = kXStages + kXStagesXtra;
+  static constexpr int kABufs = kConvert ? kXStagesMax : 0;
   static constexpr int kWStagesRaw = (kRingBudget - kXStages * kXBytes) / kWBytes;
   static_assert(kXStages <= kABufsMax || !kConvert, "TMEM A buffers");
   static constexpr int kWMax = PAIR ? QQQ_PAIR_WMAX : 12;
@@ -223,11 +234,13 @@ struct Cfg {
   static constexpr int kOffX = 0;  // 1024-aligned: NTOK*BK is a multiple of 2048
   static constexpr int kOffW = kOffX + kXStages * kXBytes;
   static constexpr int kOffBar = (kOffW + kWStages * kWBytes + 1023) / 1024 * 1024;
-  static constexpr int kNumBars = 2 * kXStages + 2 * kWStages + 4 + 2 * kEpiGroups;
+  static constexpr int kNumBars = 2 * kXStagesMax + 2 * kWStages + 4 + 2 * kEpiGroups;
   static constexpr int kOffSA = kOffBar + (kNumBars * 8 + 16 + 15) / 16 * 16;  // per-token scales of a tile (f64)
   static constexpr int kOffRS = kOffSA + NTOK * 8;                             // per-token code sums (int32)
   static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;  // per epilogue warp: 2 x [16 tok][32 ch] fp16
-  static constexpr int kOffPart = kOffY + kNumEpiWarps * 2048;  // per group: kPartBufs x 8 KiB split-K partial chunks
+  // per group: kPartBufs x 8 KiB split-K partial chunks (1024-aligned when it doubles as an activation stage)
+  static constexpr int kOffPart = kXStagesXtra ? (kOffY + kNumEpiWarps * 2048 + 1023) / 1024 * 1024
+                                               : kOffY + kNumEpiWarps * 2048;
   static constexpr int kSmemBytes = kOffPart + kEpiGroups * kPartBufs * 8192 + 1024;  // +1024 alignment slack
   static_assert(kSmemBytes <= kSmemBudget + 1024 && kSmemBytes * kCtasPerSm <= 227 * 1024,
                 "over the per-CTA shared memory budget");
@@ -732,8 +745,8 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* kb_full = bars;                   // [kXStages] activations landed + A buffer converted
-  uint64_t* kb_empty = kb_full + C::kXStages;  // [kXStages] MMA done with activation stage / A buffer
-  uint64_t* w_full = kb_empty + C::kXStages;
+  uint64_t* kb_empty = kb_full + C::kXStagesMax;  // [kXStages] MMA done with activation stage / A buffer
+  uint64_t* w_full = kb_empty + C::kXStagesMax;
   uint64_t* w_empty = w_full + C::kWStages;
   uint64_t* acc_full = w_empty + C::kWStages;
   uint64_t* acc_empty = acc_full + 2;
@@ -762,7 +775,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     }
 #endif
     griddep_launch_dependents();
-    for (int s = 0; s < C::kXStages; ++s) {
+    for (int s = 0; s < C::kXStagesMax; ++s) {
       mbar_init(&kb_full[s], C::kConvert ? (PAIR ? 2 : 1) * C::kConvPerGroup + 1 : 1);
       mbar_init(&kb_empty[s], 1);
     }
@@ -819,6 +832,11 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     cluster_sync_all();  // every cluster CTA's barriers initialised before any remote arrive / store
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // activation ring / TMEM A ring size of this launch (see Cfg::kXStagesXtra)
+  const int nx = (C::kXStagesXtra && p.aligned_tiles > 0 && p.csplit <= 1) ? C::kXStagesMax : C::kXStages;
+  auto xstage = [&](int st) -> uint8_t* {
+    return st < C::kXStages ? smem + C::kOffX + st * C::kXBytes : smem + C::kOffPart;
+  };
   // the even CTA's k-block-full and accumulator-empty barriers (pair mode)
   const uint32_t kb_full_cl = PAIR ? mapa_shared(kb_full, 0) : 0u;
   const uint32_t acc_empty_cl = PAIR ? mapa_shared(acc_empty, 0) : 0u;
@@ -952,12 +970,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             if (crank == 0) mbar_arrive_expect_tx(&kb_full[s], 2 * C::kXBytes);
             if constexpr (C::kMmaSplit == 2) {
               constexpr int kHalf = C::kTokLoad / 2;  // 96 rows per chunk
-              tma_load_3d_pair(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0 + (int)crank * kHalf,
+              tma_load_3d_pair(xstage(s), &act_map, 0, tok0 + (int)crank * kHalf,
                                kb * (BK / 128), kb_full_cl + s * 8);
-              tma_load_3d_pair(smem + C::kOffX + s * C::kXBytes + kHalf * 128, &act_map, 0,
+              tma_load_3d_pair(xstage(s) + kHalf * 128, &act_map, 0,
                                tok0 + NTOK / 2 + (int)crank * kHalf, kb * (BK / 128), kb_full_cl + s * 8);
             } else {
-              tma_load_3d_pair(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0 + (int)crank * C::kTokLoad,
+              tma_load_3d_pair(xstage(s), &act_map, 0, tok0 + (int)crank * C::kTokLoad,
                                kb * (BK / 128), kb_full_cl + s * 8);
             }
           } else {
@@ -966,11 +984,11 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
 #else
             mbar_arrive_expect_tx(&kb_full[s], C::kXBytes);
 #endif
-            tma_load_3d(smem + C::kOffX + s * C::kXBytes, &act_map, 0, tok0, kb * (BK / 128), &kb_full[s]);
+            tma_load_3d(xstage(s), &act_map, 0, tok0, kb * (BK / 128), &kb_full[s]);
           }
         }
         __syncwarp();
-        if (++s == C::kXStages) {
+        if (++s == nx) {
           s = 0;
           ph ^= 1;
         }
@@ -999,7 +1017,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
         if (lane == 0 && it < 16) QQQ_STAMP(96 + it);
         if constexpr (!C::kConvert) mma_wait(&w_full[ws], wph);
         tc_fence_after();
-        const uint32_t act_addr = smem_u32(smem + C::kOffX + xs * C::kXBytes);
+        const uint32_t act_addr = smem_u32(xstage(xs));
         const uint64_t b_desc0 = make_smem_desc(act_addr, 16, 1024, 2);
         const uint32_t a_tmem = tmem_base + C::kAccCols + xs * C::kACols;  // TMEM column address (convert modes)
         const uint32_t a_smem = smem_u32(smem + C::kOffW + ws * C::kWBytes);  // I8 mode
@@ -1032,7 +1050,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
         }
         __syncwarp();
         if (lane == 0 && it < 16) QQQ_STAMP(20 + it);
-        if (++xs == C::kXStages) {
+        if (++xs == nx) {
           xs = 0;
           xph ^= 1;
         }
@@ -1097,7 +1115,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
               ws = 0;
               wph ^= 1;
             }
-            if (++ab == C::kABufs) {
+            if (++ab == nx) {
               ab = 0;
               aph ^= 1;
             }
@@ -1210,7 +1228,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             else
               mbar_arrive(&kb_full[ab]);
           }
-          if (++ab == C::kABufs) {
+          if (++ab == nx) {
             ab = 0;
             aph ^= 1;
           }
