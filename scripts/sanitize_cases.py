@@ -63,6 +63,9 @@ def main():
         ("pair stream-K", 256, {"ntok": 256, "split": 5, "grid": 6}),
         ("pair waves + stream-K", 256, {"ntok": 256, "split": 6, "grid": 4}),
         ("ntok64 stream-K", 64, {"ntok": 64, "split": 1, "grid": 7}),
+        ("whole tiles ntok128 (4 x-stages)", 200, {"ntok": 128, "split": 0}),
+        ("cluster split-K ntok128 S=2", 100, {"ntok": 128, "split": 4, "csplit": 2}),
+        ("pair tiles ntok384", 400, {"ntok": 384, "split": 3}),
     ]
     if QUICK:
         plans = plans[:1] + plans[3:5]
@@ -112,6 +115,23 @@ def main():
         aq = P.quant_act_smoothed(torch.from_numpy(x16).cuda(), torch.from_numpy(s).cuda())
         good = np.array_equal(aq.q.cpu().numpy(), ao.q) and np.array_equal(aq.s_a.cpu().numpy(), ao.s_a)
         print(f"smoothed act quant M={m} K={k} {'OK' if good else 'MISMATCH'}", flush=True)
+        ok &= good
+    # the one-launch smoothed quantization + GEMM (qqq_w4a8_gemm_smooth_fused) against the two-kernel form
+    for tag, m, cfg in (("fused quant cluster split-K", 5, {"ntok": 16, "split": 4, "csplit": 4}),
+                        ("fused quant whole tiles", 150, {"ntok": 128, "split": 0})):
+        k, n = 2048, 512
+        rng = np.random.default_rng(9)
+        qw = Q.quant_weight_per_group(rng.standard_normal((k, n)), Q.QuantSpec("per-group", 128))
+        prep = G.prepare(qw, Q.FusedScales.from_quantized(qw))
+        s = torch.from_numpy(rng.uniform(0.5, 2.0, k)).cuda()
+        rc = Q.smoothing_reciprocal(s)
+        x = torch.from_numpy(rng.standard_normal((m, k)).astype(np.float16)).cuda()
+        aq = P.quant_act_smoothed(x, s, recip=rc)
+        y0 = G.run_gemm(aq, prep, n, False, cfg=cfg).y
+        y1, a1 = P.quant_linear_smoothed(x, s, rc, prep, n, cfg=cfg)
+        torch.cuda.synchronize()
+        good = torch.equal(y0.view(torch.int16), y1.view(torch.int16)) and torch.equal(aq.q, a1.q)
+        print(f"{tag:34s} plan={G.plan_info(prep.mode, m, n, k, cfg)} {'OK' if good else 'MISMATCH'}", flush=True)
         ok &= good
     print("ALL OK" if ok else "FAILURES", flush=True)
     return 0 if ok else 1
