@@ -438,11 +438,6 @@ QQQ_DEVICE void smooth_vecs(const GemmParams& p, int row, int slice, int gt, dou
 QQQ_DEVICE int quantize_rows_fused(const GemmParams& p, int grp, int ngroups, int gt, uint8_t* scratch, int bar_id) {
   if ((int)blockIdx.x >= p.q_ctas) return 0;
   const int wq = gt >> 5, lane = gt & 31;
-#ifdef QQQ_EXP_FQ_NOWORK
-  (void)wq;
-  (void)lane;
-  return 0;
-#endif
   const int S = (p.K + kQSlice - 1) / kQSlice;  // slices per row
   const int items = p.M * S;
   const int G = p.q_ctas * ngroups, g = grp * p.q_ctas + (int)blockIdx.x;
@@ -520,12 +515,7 @@ QQQ_DEVICE int quantize_rows_fused(const GemmParams& p, int grp, int ngroups, in
     for (int v = 0; v < 2; ++v) {
       const int64_t i = (int64_t)slice * (kQSlice / 8) + v * 128 + gt;
       if (i < nv) {
-#ifdef QQQ_EXP_FQ_NOSTORE
-        const uint2 cc = codes8_f64(xs[v], s, rs, ieee, csum);
-        if (cc.x == 0x12345678u && cc.y == 0x9abcdef0u) *reinterpret_cast<uint2*>(qr + i * 8) = cc;
-#else
         *reinterpret_cast<uint2*>(qr + i * 8) = codes8_f64(xs[v], s, rs, ieee, csum);
-#endif
       }
     }
     // codes are read by other CTAs' tensor TMA (async proxy)
@@ -568,9 +558,6 @@ QQQ_DEVICE void publish_rows_fused(const GemmParams& p, int rows, int gt, int ba
 // later async-proxy (TMA) reads after it. Co-residency: only CTAs of the first
 // wave quantize and they wait on nothing before publishing.
 QQQ_DEVICE void wait_rows_fused(const GemmParams& p) {
-#ifdef QQQ_EXP_FQ_NOWAIT
-  return;
-#endif
   const int32_t* c = p.counters + kQRowsSlot;
   unsigned long long t0 = 0;
 #pragma unroll 1
@@ -590,9 +577,6 @@ QQQ_DEVICE void wait_rows_fused(const GemmParams& p) {
 #endif
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");
-#ifdef QQQ_EXP_FUSED_SLEEP
-  { const unsigned long long t1 = gtimer(); while (gtimer() - t1 < 20000) __nanosleep(500); }
-#endif
 }
 
 // Dequant epilogue for up to 16 consecutive tokens of one output channel n:
@@ -1271,9 +1255,6 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       }
     }
     griddep_wait();  // y / acc / workspace / counters / s_a may belong to the previous kernel
-#ifdef QQQ_EXP_EPI_DELAY
-    { const unsigned long long t1 = gtimer(); while (gtimer() - t1 < QQQ_EXP_EPI_DELAY) __nanosleep(200); }
-#endif
     if (p.xsrc) {
       // fused smoothed quantization: this group's token rows, then wait for all of them
       const int gq = warp - C::kEpiWarp0;

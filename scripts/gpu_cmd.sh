@@ -1,2 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
-tail -2 gpurun_out/pytest_gpu.log; grep FAILED gpurun_out/pytest_gpu.log
+rm -f gpurun_out/c4_probe.txt
+for l in libqqq_b200 Q32 Q32R Q128; do echo "== $l" >> gpurun_out/c4_probe.txt; QQQ_LIB_PATH=paper_2406_09904_b200/lib/$l.so timeout 300 python scripts/c4_probe.py >> gpurun_out/c4_probe.txt 2>&1; done
