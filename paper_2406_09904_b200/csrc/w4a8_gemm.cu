@@ -1658,8 +1658,56 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           bulk_wait_read<0>();  // earlier contributor reductions have read the shared ring
           for (int li = 0; li < PB && li < nmine; ++li) part_issue(li);
         }
+        int li0 = 0;
+#ifndef QQQ_EPI_NO_PAIRS
+        // (single-buffered 256/384-token accumulators only, where the epilogue is
+        // serial with the next tile's MMAs; elsewhere it is overlapped and the
+        // extra registers cost more than the pairs save)
+        if (NTOK >= 256 && whole && p.y_tma && !p.acc && (!PAIR || n_tile < p.n_tiles)) {
+          // Whole tile, TMA-stored y: this warp's chunks two at a time (one TMEM
+          // load wait, one staging fence and bulk group per pair; the two 1 KiB
+          // staging buffers hold the pair, the previous pair's stores must have
+          // read them). Per-chunk latency steps were ~0.45 us of each ~0.8 us chunk.
+          uint16_t* stg0 = reinterpret_cast<uint16_t*>(ystage);
 #pragma unroll 1
-        for (int li = 0; li < nmine; ++li) {
+          for (; li0 + 1 < nmine; li0 += 2) {
+            const int c0a = (eh + H * li0) * 16, c0b = (eh + H * (li0 + 1)) * 16;
+            uint32_t ra[16], rb[16];
+            tmem_ld16x2(taddr + c0a, taddr + c0b, ra, rb);
+            if constexpr (C::kU8) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                ra[i] -= (uint32_t)rs_smem[c0a + i];  // u8 weights carried +128
+                rb[i] -= (uint32_t)rs_smem[c0b + i];
+              }
+            }
+            {  // (one chunk's halves live at a time: the kernel is at its register cap)
+              uint16_t h[16];
+              dequant16_all(ra, sa_smem + c0a, s_col, h);
+              if (lane == 0) bulk_wait_read<0>();  // the previous pair's stores have read the staging
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) stg0[i * 32 + lane] = h[i];
+              dequant16_all(rb, sa_smem + c0b, s_col, h);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) stg0[512 + i * 32 + lane] = h[i];
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&y_map, stg0, n_tile * 128 + q * 32, tok0 + c0a);
+              tma_store_2d(&y_map, stg0 + 512, n_tile * 128 + q * 32, tok0 + c0b);
+              bulk_commit();
+            }
+          }
+          if (li0 > 0) {
+            if (lane == 0) bulk_wait_read<0>();  // (the per-chunk loop alternates the buffers by ych)
+            __syncwarp();
+          }
+        }
+#endif
+#pragma unroll 1
+        for (int li = li0; li < nmine; ++li) {
           const int c0 = (eh + H * li) * 16;
           uint32_t r[16];
           tmem_ld16(taddr + c0, r);  // (includes tcgen05.wait::ld)
