@@ -80,9 +80,10 @@ def test_fused_every_plan():
         qw, fused, prep = _weights(k, n, scheme, 5)
         s = _smoothing(k, 3, frac=1)  # every channel smoothed
         recip = Q.smoothing_reciprocal(s)
-        for m in (7, 100, 333):
+        for m in (7, 100, 333, 1100):
             x = (torch.randn((m, k), generator=torch.Generator().manual_seed(m)) * 2).to(torch.float16).cuda()
-            for cfg in cfgs:
+            for cfg in (cfgs if m < 1000 else [None, {"ntok": 384, "split": 3}, {"ntok": 256, "split": 3},
+                                               {"ntok": 128, "split": 0}]):
                 _check(x, s, recip, prep, n, cfg, (scheme, m, cfg, G.plan_info(prep.mode, m, n, k, cfg)))
 
 
