@@ -1663,7 +1663,10 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
         // (single-buffered 256/384-token accumulators only, where the epilogue is
         // serial with the next tile's MMAs; elsewhere it is overlapped and the
         // extra registers cost more than the pairs save)
-        if (NTOK >= 256 && whole && p.y_tma && !p.acc && (!PAIR || n_tile < p.n_tiles)) {
+#ifndef QQQ_EPI_PAIRS_MIN_NTOK
+#define QQQ_EPI_PAIRS_MIN_NTOK 256
+#endif
+        if (NTOK >= QQQ_EPI_PAIRS_MIN_NTOK && whole && p.y_tma && !p.acc && (!PAIR || n_tile < p.n_tiles)) {
           // Whole tile, TMA-stored y: this warp's chunks two at a time (one TMEM
           // load wait, one staging fence and bulk group per pair; the two 1 KiB
           // staging buffers hold the pair, the previous pair's stores must have
