@@ -2128,10 +2128,16 @@ static double plan_cost_us(const LaunchPlan& lp, int64_t M) {
     // 2-CTA pair tiles: ~0.41 us per 128-deep k-block of a 256x256 pair tile; the
     // 192-token pair tile double-buffers its accumulator, so only the last tile's
     // epilogue is exposed (per-k-block time scaled by the MMA width, 192/256)
-    const double kT0p = 1.41, kUp = 0.4133;
+    // (x kPairF: the paired epilogue chunks took 5-8% off the 256/384-token pair
+    //  tiles after the fit; e.g. 4096x22016 M=256: pair tiles 30.6 us against the
+    //  33.0 of the stream-K plan the unscaled model preferred)
+#ifndef QQQ_PAIR_COST_F
+#define QQQ_PAIR_COST_F 0.93
+#endif
+    const double kT0p = 1.41, kUp = 0.4133, kPairF = QQQ_PAIR_COST_F;
     const double tiles_pp = lp.aligned_tiles > 0 ? (double)lp.aligned_tiles : (double)lp.units / lp.kb_per_tile / (lp.grid / 2);
     if (lp.ntok == 192) return kT0p + tiles_pp * lp.kb_per_tile * kUp * 0.78 + epi;
-    return kT0p + tiles_pp * lp.kb_per_tile * kUp + tiles_pp * epi;
+    return kPairF * (kT0p + tiles_pp * lp.kb_per_tile * kUp + tiles_pp * epi);
   }
   if (lp.aligned_tiles > 0) return T0 + ucta * u + lp.aligned_tiles * epi;
   return T0 + ucta * u + kF0 + kF1 * mt + epi;
