@@ -167,10 +167,11 @@ int qqq_w4a8_gemm_pg(const int8_t* aq, int64_t ldq, const double* s_a, const int
  * s_col == NULL is gemm_i8_i32 (gemm.py:145-154, acc only). */
 typedef struct qqq_gemm_config {
   int ntok;  /* tokens per UMMA tile: 16/32/64/128/192/256/384, 0 = auto (192, 384: pair plans
-             * only; 384 = two N=192 MMAs per K step, split 3 forced) */
+             * only; 384 = two N=192 MMAs per K step, split 3 forced; 128 with
+             * split 3: 128-token pair tiles) */
   int grid;  /* CTAs for stream-K, 0 = auto */
   int split; /* -1 auto, 0 whole tiles, 1 stream-K, 2 whole-tile waves + stream-K remainder,
-              * 3 whole 256-channel pair tiles (2-CTA clusters, ntok 256, 192 or 384), 4 cluster
+              * 3 whole 256-channel pair tiles (2-CTA clusters, ntok 256, 192, 384 or 128), 4 cluster
               * split-K (one tile per cluster, DSMEM reduction: ntok 16/32 half-SM CTAs,
               * reduce-scatter by channel rows; ntok 128 whole-SM CTAs, by token range),
               * 5 stream-K over pair tiles, 6 pair-tile waves + stream-K remainder */
