@@ -314,7 +314,10 @@ QQQ_DEVICE void st_async_b32(uint32_t cl_addr, uint32_t v, uint32_t cl_bar) {
 // peer's shared memory, completing on its mbarrier) and their code sums (into
 // rank 0, which writes s_a and rowsum). Same arithmetic as the row kernel.
 template <int kThreads, bool kSmooth, int kVPT = 1>
-__global__ void __launch_bounds__(kThreads) act_quant_cluster_kernel(const __half* __restrict__ x, int64_t K,
+#ifndef QQQ_QCLUSTER_MINB
+#define QQQ_QCLUSTER_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, QQQ_QCLUSTER_MINB) act_quant_cluster_kernel(const __half* __restrict__ x, int64_t K,
                                                                       int64_t ldx, int8_t* __restrict__ q, int64_t ldq,
                                                                       double* __restrict__ s_out, int32_t* status,
                                                                       int32_t* __restrict__ rowsum_out,
