@@ -863,12 +863,14 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       if (++wi == C::kWStages) wi = 0;
     }
     griddep_wait();  // the int8 activations come from the previous kernel
+    if (lane == 0) QQQ_STAMP(3);
     if (p.xsrc) {  // ... or from this kernel's fused quantization
       if (lane == 0) wait_rows_fused(p);
       __syncwarp();
       if (lane == 0) QQQ_STAMP(180);
     }
     for (int i = 0; i < C::kXStages && i < total; ++i) issue_x();
+    if (lane == 0) QQQ_STAMP(181);
     uint32_t ws = 0, wph = 0, xs = 0, xph = 0;
 #pragma unroll 1
     for (int i = 0; i < total; ++i) {

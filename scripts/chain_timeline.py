@@ -80,7 +80,7 @@ print(f"{a.shape} M={a.m} {a.scheme} plan={info} chain={L} graph {s.elapsed_time
       f"({s.elapsed_time(e) * 1e3 / L:.2f} us/GEMM incl. first-launch latency)")
 ds = [d.cpu().numpy().astype(np.int64) for d in dbgs]
 t0 = min(d[d[:, 0] > 0, 0].min() for d in ds)
-SLOTS = [("start", 0), ("dep_wait", 3), ("full0", 4), ("conv0", 80), ("mma_xfull0", 96), ("mma0", 20), ("mma3", 23), ("conv3", 83),
+SLOTS = [("start", 0), ("dep_wait", 3), ("x_issued", 181), ("full0", 4), ("conv0", 80), ("mma_xfull0", 96), ("mma0", 20), ("mma3", 23), ("conv3", 83),
          ("accfull0", 36), ("cs_own", 150), ("cs_recv", 151), ("cs_add", 152), ("cs_done", 153), ("loop_end", 154), ("epi_end", 63), ("exit", 42)]
 if a.fused:
     SLOTS = [("start", 0), ("q_start", 176), ("q_phaseA", 177), ("q_phaseB", 178), ("q_all", 179), ("x_wait", 180),
