@@ -177,7 +177,16 @@ struct Cfg {
 #define QQQ_BIG_PARTBUFS 2
 #endif
   static constexpr int kPartBufs = (kEpiGroups > 2 && NTOK >= 256) ? 1 : kSmall ? 2 : QQQ_BIG_PARTBUFS;  // (part_full holds 2 per group)
-  static constexpr int kEpiSmem = kNumEpiWarps * 2048 + kEpiGroups * kPartBufs * 8192;  // y staging + partial ring
+  // y staging per epilogue warp: kYBufs x [16 tok][32 ch] fp16 (1 KiB each); the
+  // whole-SM 128-token tile single-buffers it (the 12 KiB buy its activation
+  // ring one more stage), the paired epilogue chunks of 256/384-token tiles
+  // and the half-SM CTAs keep two
+#ifndef QQQ_BIG128_YBUFS
+#define QQQ_BIG128_YBUFS 1
+#endif
+  static constexpr int kYBufs = (!kSmall && !PAIR && NTOK == 128) ? QQQ_BIG128_YBUFS : 2;
+  static constexpr int kYWarpBytes = kYBufs * 1024;
+  static constexpr int kEpiSmem = kNumEpiWarps * kYWarpBytes + kEpiGroups * kPartBufs * 8192;  // y staging + partial ring
   // Two rings. Weights: their own TMA ring (released by the converters once
   // the packed bytes are consumed, or by the MMA in I8 mode). K-blocks: ring
   // slot s = activation stage s = TMEM A buffer s, guarded by ONE full barrier
@@ -239,8 +248,8 @@ struct Cfg {
   static constexpr int kOffRS = kOffSA + NTOK * 8;                             // per-token code sums (int32)
   static constexpr int kOffY = (kOffRS + NTOK * 4 + 127) / 128 * 128;  // per epilogue warp: 2 x [16 tok][32 ch] fp16
   // per group: kPartBufs x 8 KiB split-K partial chunks (1024-aligned when it doubles as an activation stage)
-  static constexpr int kOffPart = kXStagesXtra ? (kOffY + kNumEpiWarps * 2048 + 1023) / 1024 * 1024
-                                               : kOffY + kNumEpiWarps * 2048;
+  static constexpr int kOffPart = kXStagesXtra ? (kOffY + kNumEpiWarps * kYWarpBytes + 1023) / 1024 * 1024
+                                               : kOffY + kNumEpiWarps * kYWarpBytes;
   static constexpr int kSmemBytes = kOffPart + kEpiGroups * kPartBufs * 8192 + 1024;  // +1024 alignment slack
   static_assert(kSmemBytes <= kSmemBudget + 1024 && kSmemBytes * kCtasPerSm <= 227 * 1024,
                 "over the per-CTA shared memory budget");
@@ -1262,7 +1271,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
       const int gq = warp - C::kEpiWarp0;
       const int grp = gq >> 2, gt = (gq & 3) * 32 + lane;
       if (threadIdx.x == C::kEpiWarp0 * 32) QQQ_STAMP(176);
-      const int rows = quantize_rows_fused(p, grp, C::kEpiGroups, gt, smem + C::kOffY + (grp * 4) * 2048, 2 + grp);
+      const int rows = quantize_rows_fused(p, grp, C::kEpiGroups, gt, smem + C::kOffY + (grp * 4) * C::kYWarpBytes, 2 + grp);
       if (threadIdx.x == C::kEpiWarp0 * 32) QQQ_STAMP(178);
       publish_rows_fused(p, rows, gt, 2 + grp);
       if (threadIdx.x == C::kEpiWarp0 * 32) wait_rows_fused(p);
@@ -1276,7 +1285,7 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
     constexpr int kAll = C::kNumEpiWarps * 32, kHalf = kAll / H;
     double* sa_smem = reinterpret_cast<double*>(smem + C::kOffSA);
     int32_t* rs_smem = reinterpret_cast<int32_t*>(smem + C::kOffRS);
-    uint8_t* ystage = smem + C::kOffY + (warp - C::kEpiWarp0) * 2048;  // per warp: 2 x [16 tok][32 ch] fp16
+    uint8_t* ystage = smem + C::kOffY + (warp - C::kEpiWarp0) * C::kYWarpBytes;  // per warp: kYBufs x [16 tok][32 ch] fp16
     constexpr int PB = C::kPartBufs;
     uint8_t* pstage = smem + C::kOffPart + eh * (PB * 8192);
     uint64_t* pfull = part_full + 2 * eh;
@@ -1546,10 +1555,12 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
             }
             store_outputs(p, r, sa_smem + c0, tok0 + c0, tvalid - c0, n, n_ok, s_col);
             if (p.y_tma) {
-              uint16_t* stg = reinterpret_cast<uint16_t*>(ystage) + (ych & 1) * 512;
+              uint16_t* stg = reinterpret_cast<uint16_t*>(ystage) + (C::kYBufs == 2 ? (ych & 1) * 512 : 0);
               uint16_t h[16];
               dequant16_all(r, sa_smem + c0, s_col, h);
-              if (lane == 0) bulk_wait_read<1>();
+              if (lane == 0) {
+                if constexpr (C::kYBufs == 2) bulk_wait_read<1>(); else bulk_wait_read<0>();
+              }
               __syncwarp();
 #pragma unroll
               for (int i = 0; i < 16; ++i) stg[i * 32 + lane] = h[i];
@@ -1668,7 +1679,8 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
 #ifndef QQQ_EPI_PAIRS_MIN_NTOK
 #define QQQ_EPI_PAIRS_MIN_NTOK 256
 #endif
-        if (NTOK >= QQQ_EPI_PAIRS_MIN_NTOK && whole && p.y_tma && !p.acc && (!PAIR || n_tile < p.n_tiles)) {
+        if (NTOK >= QQQ_EPI_PAIRS_MIN_NTOK && C::kYBufs == 2 && whole && p.y_tma && !p.acc &&
+            (!PAIR || n_tile < p.n_tiles)) {
           // Whole tile, TMA-stored y: this warp's chunks two at a time (one TMEM
           // load wait, one staging fence and bulk group per pair; the two 1 KiB
           // staging buffers hold the pair, the previous pair's stores must have
@@ -1739,11 +1751,13 @@ __global__ void __launch_bounds__(Cfg<MODE, NTOK, BK, PAIR>::kNumThreads, Cfg<MO
           if (p.y_tma && (!PAIR || n_tile < p.n_tiles)) {
             // y chunk -> this warp's staging [16 tok][32 ch] fp16 -> its own TMA store
             // (OOB rows/cols clipped): no cross-warp barrier on the store path
-            uint16_t* stg = reinterpret_cast<uint16_t*>(ystage) + (ych & 1) * 512;
+            uint16_t* stg = reinterpret_cast<uint16_t*>(ystage) + (C::kYBufs == 2 ? (ych & 1) * 512 : 0);
             uint16_t h[16];
             dequant16_all(r, sa_smem + c0, s_col, h);
             if (lead && seg == 0 && li < 4) QQQ_STAMP(128 + li);
-            if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer two chunks ago has read it
+            if (lane == 0) {  // the store that used this buffer (two chunks ago; one with a single buffer) has read it
+              if constexpr (C::kYBufs == 2) bulk_wait_read<1>(); else bulk_wait_read<0>();
+            }
             __syncwarp();
             if (lead && seg == 0 && li < 4) QQQ_STAMP(132 + li);
 #pragma unroll
