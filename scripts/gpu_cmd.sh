@@ -1,1 +1,4 @@
-timeout 900 python scripts/quick_bench.py --ms 768,1024 --shapes 11008x4096,4096x4096,4096x11008 --cfgs 'auto;{"ntok":256,"split":3};{"ntok":256,"split":5};{"ntok":256,"split":6};{"ntok":384,"split":3};{"ntok":192,"split":3};{"ntok":192,"split":5}' > gpurun_out/qb.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+tail -2 gpurun_out/pytest_gpu.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
